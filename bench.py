@@ -1,0 +1,497 @@
+#!/usr/bin/env python3
+"""Benchmark of the approximate-region hot path (BASELINE.json metric:
+"approx-region items/s & speedup vs exact GPU kernel at <=1% quality loss").
+
+Default workload (configs[1]): Binomial options, 1,048,576 American puts x
+1024-step CRR lattice under team-shared iACT input memoization
+(memo(in:...) level(team), kPerTeam mapping, 64-thread teams). One step =
+one pass of the region over the whole portfolio with inputs resident in
+HBM. Per-GPU work is fixed (weak scaling): each rank prices its own
+1,048,576-option shard; no collective on the data path.
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
+  python bench.py [--gpus N --steps K --warmup W] [--workload binomial|blackscholes|kmeans]
+  python bench.py --impl reference ...   # the reference's CPU engine (oracle/_ref)
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "approx-region items/s & speedup vs exact GPU kernel at <=1% quality loss"
+
+# Workload definitions (the N=1 headline is "binomial").
+WORKLOADS = {
+    "binomial": dict(
+        name="binomial-1M-x-1024-iact-team",
+        benchmark="binomial", n=1 << 20, lattice=1024, ipt=128,
+        directive="memo(in:4:0.5) level(team)", spec=("iact", 4, 0.5, None, "team"),
+        unit="options/s"),
+    "blackscholes": dict(
+        name="blackscholes-4M-taf-h5", benchmark="blackscholes", n=1 << 22, ipt=16,
+        directive="memo(out:5:1:0.5)", spec=("taf", 5, 1, 0.5, "thread"), unit="options/s"),
+    "kmeans": dict(
+        name="kmeans-16M-x-32-x-64-perfo-small", benchmark="kmeans", n=1 << 24, dims=32, k=64,
+        ipt=4, directive="perfo(small:2)", spec=("perfo", "small", 2), unit="point-iterations/s"),
+}
+
+# Algorithmic work per item: binomial lattice FP64 flops
+# per evaluated option = 5 per node x N(N+1)/2 nodes.
+def binomial_flops(N):
+    return 5.0 * N * (N + 1) / 2.0
+
+
+def kmeans_flops(d, k):
+    return 3.0 * d * k + k  # sub, mul, add per (c, d) + sqrt per centroid
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def load_traffic(workload):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(workload)
+        except Exception:
+            return None
+    return None
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            pass
+    return {}
+
+
+def make_spec(E, s):
+    if s[0] == "iact":
+        return E.iact(s[1], s[2], s[3], s[4])
+    if s[0] == "taf":
+        return E.taf(s[1], s[2], s[3], s[4])
+    return E.perfo(s[1], s[2])
+
+
+# ------------------------------------------------------------------ reference arm
+
+def reference_arm(args, wl):
+    """The reference's own CPU engine (oracle/_ref = /root/reference compiled),
+    on all host threads, on bounded samples of the same workload."""
+    import numpy as np
+
+    import oracle
+    from paper_2308_16877_b200 import engine as E
+
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    lib = oracle.ref()
+    cores = os.cpu_count() or 1
+    n = wl["n"]
+    if wl["benchmark"] == "binomial":
+        opts = E.make_binomial_portfolio(n, 42)
+        grid, mapping = E.resolve_grid("binomial", n, items_per_thread=wl["ipt"])
+        T = grid.num_teams
+        per_team = 2  # options of one team per worker and step (669 ms each in-engine)
+        sample_desc = (f"{cores} threads x 1 team x {per_team} options (idx = team + s*{T}), "
+                       f"{wl['lattice']}-step lattice, reference run_region per team")
+
+        def work(worker, step):
+            team = (worker * 97 + step * 13) % T
+            idx = team + np.arange(per_team) * T
+            sub = np.ascontiguousarray(opts[idx])
+            out = np.zeros(per_team)
+            g = E.GridConfig(1, 64, 32, per_team)
+            reg = E.binomial_region(sub, wl["lattice"], out)
+            rc, st, msg = oracle.ref_run(g, per_team, 1, reg, make_spec(E, wl["spec"]))
+            assert rc == 0, msg
+            return per_team
+    elif wl["benchmark"] == "blackscholes":
+        opts = E.make_bs_portfolio(1 << 20, 42)
+        per = 1 << 16
+        sample_desc = f"{cores} threads x {per} options (1024 teams x 64, ipt 1), reference run_region"
+
+        def work(worker, step):
+            lo = ((worker + step * cores) * per) % (1 << 20)
+            sub = np.ascontiguousarray(opts[lo:lo + per])
+            out = np.zeros(per)
+            g = E.GridConfig(per // 64 // 16, 64, 32, 16)
+            rc, st, msg = oracle.ref_run(g, per, 0, E.blackscholes_region(sub, out), make_spec(E, wl["spec"]))
+            assert rc == 0, msg
+            return per
+    else:
+        d, k = wl["dims"], wl["k"]
+        per = 1 << 12
+        pts = E.make_blobs(per * 4, d, k, 42, 8.0)
+        cents = pts[:k].copy()
+        sample_desc = f"{cores} threads x {per} points x {d} dims x {k} clusters, one region launch"
+
+        def work(worker, step):
+            lo = ((worker + step) % 4) * per
+            sub = np.ascontiguousarray(pts[lo:lo + per])
+            lab = np.zeros(per, np.int32)
+            g = E.GridConfig(per // 256, 64, 32, 4)
+            rc, st, msg = oracle.ref_run(g, per, 0, E.kmeans_region(sub, cents, lab), make_spec(E, wl["spec"]))
+            assert rc == 0, msg
+            return per
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one_step(step):
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            return sum(ex.map(lambda w: work(w, step), range(cores)))
+
+    for s in range(args.warmup):
+        one_step(-1 - s)
+    t0 = time.perf_counter()
+    items = 0
+    for s in range(args.steps):
+        items += one_step(s)
+    dt = time.perf_counter() - t0
+    value = items / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": wl["unit"],
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / max(1, args.steps) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "directive": wl["directive"]},
+        "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": "reference",
+                         "sample": sample_desc},
+        "e2e": {"value": value, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def cpu_baseline_sample(wl, opts, grid):
+    """Reference CPU engine on rank 0, one thread, bounded sample (~10-20 s)."""
+    import numpy as np
+
+    import oracle
+    from paper_2308_16877_b200 import engine as E
+    try:
+        lib = oracle.ref()
+        kind = "reference"
+        runner = oracle.ref_run
+    except Exception:
+        kind = "port"
+        runner = oracle.oracle_run
+    t0 = time.perf_counter()
+    if wl["benchmark"] == "binomial":
+        T = grid.num_teams
+        m = 16
+        idx = 0 + np.arange(m) * T
+        sub = np.ascontiguousarray(opts[idx])
+        out = np.zeros(m)
+        rc, st, msg = runner(E.GridConfig(1, 64, 32, m), m, 1, E.binomial_region(sub, wl["lattice"], out),
+                             make_spec(E, wl["spec"]))
+        items = m
+        desc = f"team 0: {m} options (idx = s*{T}), {wl['lattice']}-step lattice, 1 thread"
+    elif wl["benchmark"] == "blackscholes":
+        m = 1 << 20
+        sub = np.ascontiguousarray(opts[:m])
+        out = np.zeros(m)
+        rc, st, msg = runner(E.GridConfig(1024, 64, 32, 16), m, 0, E.blackscholes_region(sub, out),
+                             make_spec(E, wl["spec"]))
+        items = m
+        desc = f"first {m} options, 1024 teams x 64 x ipt 16, 1 thread"
+    else:
+        m = 1 << 14
+        pts = np.ascontiguousarray(opts[0][:m])
+        lab = np.zeros(m, np.int32)
+        rc, st, msg = runner(E.GridConfig(m // 256, 64, 32, 4), m, 0, E.kmeans_region(pts, opts[1], lab),
+                             make_spec(E, wl["spec"]))
+        items = m
+        desc = f"{m} points, one region launch, 1 thread"
+    dt = time.perf_counter() - t0
+    return {"value": items / dt, "unit": wl["unit"], "cores": 1, "kind": kind, "sample": desc}
+
+
+def our_arm(args, wl):
+    import numpy as np
+    import torch
+
+    from paper_2308_16877_b200 import abi
+    from paper_2308_16877_b200 import engine as E
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    n = wl["n"]
+    spec = make_spec(E, wl["spec"])
+
+    # ---- inputs (synthetic, seeded; each rank its own shard of a ws*n job)
+    seed = 42 + rank
+    if wl["benchmark"] == "binomial":
+        opts = E.make_binomial_portfolio(n, seed)
+        grid, mapping = E.resolve_grid("binomial", n, items_per_thread=wl["ipt"])
+        d_in = torch.from_numpy(opts).to(dev)
+        out_exact = torch.zeros(n, dtype=torch.float64, device=dev)
+        out = torch.zeros(n, dtype=torch.float64, device=dev)
+        mk = lambda o, s=None: E.binomial_region(d_in, wl["lattice"], o)
+        h2d_bytes, d2h_bytes = n * 40, n * 8
+        flops_item = binomial_flops(wl["lattice"])
+        bound = "fp64"
+        cpu_inputs = opts
+    elif wl["benchmark"] == "blackscholes":
+        opts = E.make_bs_portfolio(n, seed)
+        grid, mapping = E.resolve_grid("blackscholes", n, items_per_thread=wl["ipt"])
+        d_in = torch.from_numpy(opts).to(dev)
+        out_exact = torch.zeros(n, dtype=torch.float64, device=dev)
+        out = torch.zeros(n, dtype=torch.float64, device=dev)
+        mk = lambda o, s=None: E.blackscholes_region(d_in, o)
+        h2d_bytes, d2h_bytes = n * 40, n * 8
+        flops_item = None
+        bound = "hbm"
+        cpu_inputs = opts
+    else:
+        d, k = wl["dims"], wl["k"]
+        pts = E.make_blobs(n, d, k, seed, 8.0)
+        cents = pts[:k].copy()
+        grid, mapping = E.resolve_grid("kmeans", n, items_per_thread=wl["ipt"])
+        d_in = torch.from_numpy(pts).to(dev)
+        d_c = torch.from_numpy(cents).to(dev)
+        out_exact = torch.zeros(n, dtype=torch.int32, device=dev)
+        out = torch.zeros(n, dtype=torch.int32, device=dev)
+        mk = lambda o, s=None: E.kmeans_region(d_in, d_c, o)
+        h2d_bytes, d2h_bytes = n * d * 8, n * 4
+        flops_item = kmeans_flops(d, k)
+        bound = "fp64"
+        cpu_inputs = (pts, cents)
+
+    # L2 flush buffer (> 126 MB L2), written between timed iterations
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def timed_run(target, sp, steps, warmup):
+        ts = []
+        stats = None
+        for i in range(warmup + steps):
+            flush.zero_()
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            lr = E.run_region(grid, n, mapping, mk(target), sp, stream=stream, synchronous=False)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            st = abi.Stats()
+            rc = abi.lib().hpac_stats_fetch(C.byref(st))
+            assert rc == 0, rc
+            if i >= warmup:
+                ts.append(ev0.elapsed_time(ev1))
+                stats = st.as_dict()
+        return ts, stats
+
+    # exact GPU kernel (same grid, spec = NULL) and the approximate region
+    ts_exact, st_exact = timed_run(out_exact, None, args.steps, args.warmup)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ts_apx, st_apx = timed_run(out, spec, args.steps, args.warmup)
+    clk = clocks.stop()
+
+    # quality loss (application metric) vs the exact run
+    if wl["benchmark"] == "kmeans":
+        quality = {"mcr": E.mcr(out_exact, out)}
+        qv = quality["mcr"]
+    else:
+        quality = {"mape": E.mape(out_exact, out)}
+        qv = quality["mape"]
+
+    t_apx = sum(ts_apx)
+    t_exact = sum(ts_exact)
+    if dist is not None:
+        t = torch.tensor([t_apx, t_exact], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_apx, t_exact = t.tolist()
+    value = ws * n * args.steps / (t_apx * 1e-3)
+    exact_value = ws * n * args.steps / (t_exact * 1e-3)
+    ms_per_step = t_apx / args.steps
+
+    # ---- end to end through the C-ABI with pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        if wl["benchmark"] == "kmeans":
+            h_in = torch.from_numpy(pts).pin_memory()
+            h_lab = torch.zeros(n, dtype=torch.int32).pin_memory()
+            hreg = E.kmeans_region(h_in.numpy(), cents, h_lab.numpy())
+        else:
+            h_in = torch.from_numpy(cpu_inputs).pin_memory()
+            h_out = torch.zeros(n, dtype=torch.float64).pin_memory()
+            hreg = (E.binomial_region(h_in.numpy(), wl["lattice"], h_out.numpy())
+                    if wl["benchmark"] == "binomial" else E.blackscholes_region(h_in.numpy(), h_out.numpy()))
+        E.run_region_host(grid, n, mapping, hreg, spec)  # warm-up
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            E.run_region_host(grid, n, mapping, hreg, spec)
+        e2e_t = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = t.item()
+        e2e = {"value": ws * n * args.e2e_steps / e2e_t, "unit": wl["unit"],
+               "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+               "steps": args.e2e_steps}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (the region kernel itself)
+    peaks = measured_peaks()
+    avg_ms = t_apx / args.steps
+    if bound == "fp64":
+        fp = C.c_double()
+        abi.lib().hpac_probe_fp64_peak(C.byref(fp))
+        evaluated = st_apx["total_invocations"] - st_apx["approx_invocations"]
+        per_item_lanes = grid.threads_per_team if mapping == 1 else 1
+        evaluated_items = evaluated / per_item_lanes
+        achieved = evaluated_items * flops_item / (avg_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": fp.value, "unit": "TFLOP/s",
+                "frac": achieved / fp.value if fp.value else None,
+                "peak_source": "in-run DFMA probe (hpac_probe_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
+                "algorithmic": f"{flops_item:.4g} FP64 flops per evaluated item"}
+    else:
+        approx_items = st_apx["approx_invocations"]
+        bytes_launch = 48 * n - 40 * approx_items  # approx items skip the 40 B input read
+        achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
+                "algorithmic": "48 B per exact option, 8 B per TAF-approximated option"}
+    roof["traffic"] = load_traffic(wl["name"])
+
+    cpu = None
+    if args.cpu_baseline and ws == 1:
+        try:
+            cpu = cpu_baseline_sample(wl, cpu_inputs, grid)
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "unit": wl["unit"], "cores": 1, "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": wl["unit"], "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators, seed 42 + rank)",
+        "config": {"workload": wl["name"], "n_per_gpu": n, "directive": wl["directive"],
+                   "grid": {"num_teams": grid.num_teams, "threads_per_team": grid.threads_per_team,
+                            "warp_size": grid.warp_size, "items_per_thread": grid.items_per_thread},
+                   "mapping": "per-team" if mapping == 1 else "per-thread",
+                   "lattice_steps": wl.get("lattice"), "l2": "flushed between timed iterations",
+                   "parallelism": f"dp{ws} (independent shards)"},
+        "speedup_vs_exact": value / exact_value,
+        "exact_value": exact_value,
+        "quality": quality, "quality_ok": bool(qv <= 0.01),
+        "approx_rate": st_apx["approx_invocations"] / max(1, st_apx["total_invocations"]),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": args.steps, "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="binomial", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        reference_arm(args, wl)
+    else:
+        our_arm(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,700 @@
+// engine_team.cu — the approximate-region engine for the per-team work
+// mapping (WorkMapping::kPerTeam, grid.hpp:14): every thread of a logical
+// team works on the same item (engine.hpp:198, machine.hpp:77-80).
+//
+// Key property (verified there on the reference): under
+// per-team mapping every lane of a team sees the same input, the same
+// outputs and therefore the same technique state, so every predicate and
+// every vote is team-uniform; iACT writer choice is the lowest lane and all
+// of a team's tables hold identical entries. The engine therefore keeps ONE
+// decision state per team (a team-shared iACT table, one TAF window, one
+// perforation counter) and scales the lane-level statistics by the team
+// shape: total/approx invocations x threads_per_team, warp steps x
+// warps_per_team, zero divergence, uniform barrier arrivals. Results,
+// decisions and stats equal the reference's lane-by-lane execution.
+//
+// Two kernels:
+//  * engine_team_seq_kernel: apps whose evaluate is a scalar function
+//    (TABLE / SYNTHETIC / BLACKSCHOLES); one CUDA thread runs one team.
+//  * binomial_team_kernel: the CRR lattice (bench/binomial.hpp:16-50) is
+//    evaluated cooperatively by a warp with a register-blocked, rebalanced
+//    lattice; iACT / perforation decisions depend on inputs only, so the
+//    team first decides a chunk of its items, then its warps evaluate the
+//    misses in parallel and hits are resolved from the producing step.
+#include <cuda_runtime.h>
+
+#include "apps.cuh"
+#include "engine.h"
+#include "hpac_device.cuh"
+
+namespace hpac {
+
+constexpr int kTechNoneT = 3;
+
+namespace {
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void flush_stats(const EngineParams& p, unsigned long long tot,
+                                            unsigned long long app, unsigned long long ws,
+                                            unsigned long long res, bool err) {
+  tot = warp_sum(tot);
+  app = warp_sum(app);
+  ws = warp_sum(ws);
+  res = warp_sum(res);
+  unsigned e = __ballot_sync(0xffffffffu, err);
+  if ((threadIdx.x & 31) == 0) {
+    if (tot) atomicAdd(&p.counters[kCntTotal], tot);
+    if (app) atomicAdd(&p.counters[kCntApprox], app);
+    if (ws) atomicAdd(&p.counters[kCntWarpSteps], ws);
+    if (res) atomicAdd(&p.counters[kCntResidentWarps], res);
+    if (e) atomicAdd(&p.counters[kCntAppError], 1ull);
+  }
+}
+
+// Team-shared iACT lookup (MemoTable::lookup / nearest_slot, iact.hpp:93-122)
+// over `occ` slots of a table stored as tab[(slot*D + c) * stride].
+__device__ __forceinline__ void team_lookup(const double* tab, int stride, int D, int in_dims,
+                                            const double* in, int occ, double thr, int& hit,
+                                            int& near) {
+  double hit_d = 0.0, near_d = dinf();
+  hit = -1;
+  near = -1;
+  for (int s = 0; s < occ; ++s) {
+    double ssq = 0.0;
+    for (int c = 0; c < in_dims; ++c) {
+      double df = __dsub_rn(tab[(s * D + c) * stride], in[c]);
+      ssq = __dadd_rn(ssq, __dmul_rn(df, df));
+    }
+    double dd = __dsqrt_rn(ssq);
+    if (dd <= thr && (hit < 0 || dd < hit_d)) {
+      hit = s;
+      hit_d = dd;
+    }
+    if (dd < near_d) {
+      near_d = dd;
+      near = s;
+    }
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// Scalar apps under per-team mapping: one CUDA thread = one logical team.
+// ===========================================================================
+template <class App, int TECH, int HREG>
+__global__ void __launch_bounds__(128) engine_team_seq_kernel(const EngineParams p, int team_end) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int IN_MAX = App::IN_MAX;
+  constexpr int OUT_MAX = App::OUT_MAX;
+  const int team = p.team_begin + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  const bool live = team < team_end;
+  const int stride_s = blockDim.x;
+  double* ring = smem + p.smem_taf_off;  // [(d*h + slot) * blockDim + t]
+  double* tab = smem + p.smem_tab_off;   // [(slot*D + c) * blockDim + t]
+  ring += threadIdx.x;
+  tab += threadIdx.x;
+  const int D = p.in_dims + p.out_dims;
+
+  int mode = kTafFilling, rem = 0, cnt = 0, head = 0;
+  double win[HREG > 0 ? HREG : 1];
+#pragma unroll
+  for (int i = 0; i < (HREG > 0 ? HREG : 1); ++i) win[i] = 0.0;
+  double last[OUT_MAX];
+#pragma unroll
+  for (int d = 0; d < OUT_MAX; ++d) last[d] = 0.0;
+  int rr = 0, occ = 0;
+  int64_t pcount = 0;
+  int64_t trip = live ? trip_count(team, p.stride, p.n, p.steps) : 0;
+
+  unsigned long long tot = 0, app = 0, wsteps = 0;
+  bool touched = false, err = false;
+  const unsigned long long tpt = (unsigned long long)p.tpt;
+  const unsigned long long wpt = (unsigned long long)p.wpt;
+
+  for (int64_t step = 0; live && step < trip; ++step) {
+    const int64_t idx = team + step * p.stride;
+    const int enc = p.has_enc ? p.region.encounters[idx] : 1;
+    uint8_t pbits = 0;
+    for (int round = 0; round < enc; ++round) {
+      double in[IN_MAX];
+      bool loaded = false, pred = false;
+      int hit = -1, near = -1;
+      if (TECH == HPAC_TECH_TAF) {
+        pred = mode == kTafPredicting;
+      } else if (TECH == HPAC_TECH_IACT) {
+        App::load(p, idx, in);
+        loaded = true;
+        team_lookup(tab, stride_s, D, p.in_dims, in, occ, p.iact_thr, hit, near);
+        pred = hit >= 0;
+      } else if (TECH == HPAC_TECH_PERFO) {
+        // per-thread and herded counters coincide under per-team mapping
+        pred = perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, pcount,
+                                 trip, team);
+      }
+      bool approx = pred;  // unanimous: every vote returns the predicate
+      double out[OUT_MAX];
+#pragma unroll
+      for (int d = 0; d < OUT_MAX; ++d) out[d] = 0.0;
+      if (approx) {
+        if (TECH == HPAC_TECH_TAF) {
+#pragma unroll
+          for (int d = 0; d < OUT_MAX; ++d) out[d] = last[d];
+          if (mode == kTafPredicting && --rem == 0) {
+            cnt = 0;
+            head = 0;
+            mode = kTafFilling;
+          }
+          App::store(p, idx, out);
+        } else if (TECH == HPAC_TECH_IACT) {
+#pragma unroll
+          for (int d = 0; d < OUT_MAX; ++d)
+            if (d < p.out_dims) out[d] = tab[(hit * D + p.in_dims + d) * stride_s];
+          App::store(p, idx, out);
+        }
+      } else {
+        if (!loaded) App::load(p, idx, in);
+        if (!App::eval(p, idx, in, out, nullptr)) err = true;
+        App::store(p, idx, out);
+        if (TECH == HPAC_TECH_TAF) {
+          bool full;
+          if (HREG > 0) {
+#pragma unroll
+            for (int i = 0; i + 1 < (HREG > 0 ? HREG : 1); ++i) win[i] = win[i + 1];
+            win[(HREG > 0 ? HREG : 1) - 1] = out[0];
+            if (cnt < HREG) ++cnt;
+            full = cnt == HREG;
+          } else {
+            const int h = p.taf_h;
+            int slot;
+            if (cnt < h) {
+              slot = head + cnt;
+              if (slot >= h) slot -= h;
+              ++cnt;
+            } else {
+              slot = head;
+              head = head + 1 == h ? 0 : head + 1;
+            }
+            for (int d = 0; d < p.out_dims; ++d) ring[(d * h + slot) * stride_s] = out[d];
+            full = cnt == h;
+          }
+#pragma unroll
+          for (int d = 0; d < OUT_MAX; ++d) last[d] = out[d];
+          if (mode == kTafPredicting) {
+            if (--rem == 0) {
+              cnt = 0;
+              head = 0;
+              mode = kTafFilling;
+            }
+          } else if ((mode == kTafFilling && full) || mode == kTafChecking) {
+            bool pass = true;
+            if (HREG > 0) {
+              pass = taf_window_passes<(HREG > 0 ? HREG : 1)>(win, p.taf_thr);
+            } else {
+              for (int d = 0; d < p.out_dims && pass; ++d)
+                pass = taf_ring_passes(ring + d * p.taf_h * stride_s, stride_s, p.taf_h, head,
+                                       cnt, p.taf_thr);
+            }
+            if (pass) {
+              rem = p.taf_p;
+              mode = kTafPredicting;
+            } else {
+              mode = kTafChecking;
+            }
+          }
+        }
+        if (TECH == HPAC_TECH_IACT) {
+          // every lane missed with the same input: the lowest lane writes
+#pragma unroll
+          for (int c = 0; c < IN_MAX; ++c)
+            if (c < p.in_dims) tab[(rr * D + c) * stride_s] = in[c];
+#pragma unroll
+          for (int d = 0; d < OUT_MAX; ++d)
+            if (d < p.out_dims) tab[(rr * D + p.in_dims + d) * stride_s] = out[d];
+          rr = rr + 1 == p.tsize ? 0 : rr + 1;
+          occ = occ + 1 < p.tsize ? occ + 1 : p.tsize;
+        }
+      }
+      if (TECH == HPAC_TECH_PERFO) pcount += 1;
+      tot += tpt;
+      wsteps += wpt;
+      touched = true;
+      if (approx) {
+        app += tpt;
+        if (round < 8) pbits |= (uint8_t)(1u << round);
+      }
+    }
+    if (p.paths) p.paths[idx] = pbits;
+  }
+  flush_stats(p, tot, app, wsteps, touched ? wpt : 0ull, err);
+}
+
+// ===========================================================================
+// Binomial options: warp-cooperative register-blocked CRR lattice.
+// ===========================================================================
+struct LatParams {
+  double K;
+  double pd, qd;  // disc * p, disc * (1 - p)
+  double up, up2, lnu, S;
+};
+
+template <bool AM, bool PUT>
+__device__ __forceinline__ double lat_node(double vl, double vr, double s, const LatParams& q) {
+  double cont = fma(q.pd, vr, q.qd * vl);
+  if (!AM) return cont;
+  double x = PUT ? q.K - s : s - q.K;
+  // cont >= +0 always, so signed-integer order on the bit patterns equals
+  // max(cont, max(x, 0)) (binomial.hpp:42-44) without an FP64-pipe compare.
+  long long ci = __double_as_longlong(cont), xi = __double_as_longlong(x);
+  return __longlong_as_double(ci > xi ? ci : xi);
+}
+
+// One phase of the lattice at block size B: lane owns nodes
+// [lane*B, lane*B + B) in registers for every level whose live nodes
+// (0..L+1) need blocks of B (L+2 > 32*(B-1)). Values enter and leave the
+// phase through this warp's shared-memory node array `xch`, which is the
+// rebalance: the next phase reads the same nodes back in smaller blocks,
+// so the triangle keeps all 32 lanes busy down to the root.
+template <int B, int BMAX, bool AM, bool PUT>
+__device__ __forceinline__ void lat_phase(double (&v)[BMAX], int& L, int B0, const LatParams& q,
+                                          int lane, double* xch) {
+  if (B > B0 || L < 0 || L + 2 <= 32 * (B - 1)) return;
+#pragma unroll
+  for (int i = 0; i < B; ++i) v[i] = xch[lane * B + i];
+  // s0 = S * up^(2*j0 - L) for this lane's first node j0 = lane*B
+  double s0 = q.S * exp((double)(2 * lane * B - L) * q.lnu);
+  while (L >= 0 && L + 2 > 32 * (B - 1)) {
+    double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+    double s = s0;
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double right = (i + 1 < B) ? v[i + 1] : vr;
+      v[i] = lat_node<AM, PUT>(v[i], right, s, q);
+      if (AM) s *= q.up2;
+    }
+    s0 *= q.up;
+    --L;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < B; ++i) xch[lane * B + i] = v[i];
+  __syncwarp();
+}
+
+template <int B, int BMAX, bool AM, bool PUT>
+__device__ __forceinline__ void lat_chain(double (&v)[BMAX], int& L, int B0, const LatParams& q,
+                                          int lane, double* xch) {
+  if constexpr (B >= 1) {
+    lat_phase<B, BMAX, AM, PUT>(v, L, B0, q, lane, xch);
+    lat_chain<B - 1, BMAX, AM, PUT>(v, L, B0, q, lane, xch);
+  }
+}
+
+// binomial_price (bench/binomial.hpp:16-50) by one warp; every lane
+// returns the price. `xch` = 32*BMAX doubles of this warp's shared memory.
+template <int BMAX, bool AM, bool PUT>
+__device__ double binomial_warp_price(const double* o, int N, double* xch, bool& ok) {
+  const int lane = threadIdx.x & 31;
+  double spot = o[0], strike = o[1], rate = o[2], vol = o[3], mat = o[4];
+  ok = true;
+  if (!(spot > 0) || !(strike > 0) || !(mat > 0) || !(vol > 0) || N < 1) {
+    ok = false;
+    return 0.0;
+  }
+  double dt = mat / N;
+  double lnu = vol * sqrt(dt);
+  double up = exp(lnu);
+  double down = 1.0 / up;
+  double growth = exp(rate * dt);
+  double pu = (growth - down) / (up - down);
+  if (!(pu > 0.0) || !(pu < 1.0)) {
+    ok = false;
+    return 0.0;
+  }
+  double disc = 1.0 / growth;
+  LatParams q;
+  q.K = strike;
+  q.pd = disc * pu;
+  q.qd = disc * (1.0 - pu);
+  q.up = up;
+  q.up2 = up * up;
+  q.lnu = lnu;
+  q.S = spot;
+  const int B0 = (N + 1 + 31) / 32;
+  // leaves: intrinsic at S * up^(2j - N), j = 0..N (nodes beyond N are dead)
+  for (int j = lane; j < 32 * B0; j += 32) {
+    double s = spot * exp((double)(2 * j - N) * lnu);
+    double x = PUT ? strike - s : s - strike;
+    xch[j] = x < 0.0 ? 0.0 : x;
+  }
+  __syncwarp();
+  double v[BMAX];
+  int L = N - 1;
+  lat_chain<BMAX, BMAX, AM, PUT>(v, L, B0, q, lane, xch);
+  double r = xch[0];
+  __syncwarp();
+  return r;
+}
+
+// Lattices beyond the register bound (N+1 > 32*33): shared-memory values,
+// warp-strided nodes, double-buffered levels (same arithmetic).
+template <bool AM, bool PUT>
+__device__ double binomial_warp_price_smem(const double* o, int N, double* buf, bool& ok) {
+  const int lane = threadIdx.x & 31;
+  double spot = o[0], strike = o[1], rate = o[2], vol = o[3], mat = o[4];
+  ok = true;
+  if (!(spot > 0) || !(strike > 0) || !(mat > 0) || !(vol > 0) || N < 1) {
+    ok = false;
+    return 0.0;
+  }
+  double dt = mat / N, lnu = vol * sqrt(dt), up = exp(lnu), down = 1.0 / up;
+  double growth = exp(rate * dt);
+  double pu = (growth - down) / (up - down);
+  if (!(pu > 0.0) || !(pu < 1.0)) {
+    ok = false;
+    return 0.0;
+  }
+  double disc = 1.0 / growth;
+  LatParams q;
+  q.K = strike;
+  q.pd = disc * pu;
+  q.qd = disc * (1.0 - pu);
+  q.up = up;
+  q.up2 = up * up;
+  q.lnu = lnu;
+  q.S = spot;
+  double* a = buf;
+  double* b = buf + (N + 2);
+  for (int j = lane; j <= N; j += 32) {
+    double s = spot * exp((double)(2 * j - N) * lnu);
+    double x = PUT ? strike - s : s - strike;
+    a[j] = x < 0.0 ? 0.0 : x;
+  }
+  __syncwarp();
+  for (int L = N - 1; L >= 0; --L) {
+    for (int j = lane; j <= L; j += 32) {
+      double s = spot * exp((double)(2 * j - L) * lnu);
+      b[j] = lat_node<AM, PUT>(a[j], a[j + 1], s, q);
+    }
+    __syncwarp();
+    double* t = a;
+    a = b;
+    b = t;
+  }
+  double r = a[0];
+  __syncwarp();
+  return r;
+}
+
+constexpr int kLatBmax = 33;  // register lattice up to N = 32*33 - 1 = 1055 steps
+constexpr int kBinoChunk = 256;
+constexpr int kBinoWarps = 2;  // = threads_per_team / 32 at the default tpt 64
+
+// Decision codes in the chunk plan.
+constexpr int kActSkip = -1;
+constexpr int kActMiss = -2;
+// >= 0: hit on a slot written in an earlier chunk -> (slot)         [kHitOld]
+// <= -3: hit on a step s of this chunk -> -(3 + s)                    [kHitNew]
+
+template <int TECH, bool AM, bool PUT>
+__global__ void __launch_bounds__(kBinoWarps * 32) binomial_team_kernel(const EngineParams p) {
+  extern __shared__ __align__(16) double smem[];
+  const int team = p.team_begin + (int)blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int N = p.region.binomial_steps;
+  const bool big = N + 1 > 32 * kLatBmax;
+
+  // shared-memory carve-up
+  double* price = smem;                        // [kBinoChunk]
+  double* slot_val = price + kBinoChunk;       // [tsize]
+  double* tab = smem + p.smem_tab_off;         // [tsize * 5] team table inputs / TAF ring
+  double* xch = smem + p.smem_scratch_off;     // [warps][32*BMAX or 2(N+2)]
+  const int xch_per_warp = big ? 2 * (N + 2) : 32 * kLatBmax;
+  xch += warp * xch_per_warp;
+  int* act = reinterpret_cast<int*>(smem + p.smem_ctl_off);  // [kBinoChunk]
+  int* miss = act + kBinoChunk;                              // [kBinoChunk]
+  int* slot_src = miss + kBinoChunk;                         // [tsize] producing step
+  int* nmiss_s = slot_src + (p.tsize > 0 ? p.tsize : 1);
+
+  const int64_t trip = trip_count(team, p.stride, p.n, p.steps);
+  int rr = 0, occ = 0;  // team table cursor (thread 0)
+  unsigned long long tot = 0, app = 0, wsteps = 0;
+  bool err = false;
+  const unsigned long long tpt = (unsigned long long)p.tpt;
+  const unsigned long long wpt = (unsigned long long)p.wpt;
+
+  // TAF under per-team binomial: sequential, evaluated by warp 0 only.
+  if (TECH == HPAC_TECH_TAF) {
+    if (warp != 0) return;
+    int mode = kTafFilling, rem = 0, cnt = 0, head = 0;
+    double lastv = 0.0;
+    double* ring = tab;  // h doubles (kept in smem; tiny)
+    for (int64_t step = 0; step < trip; ++step) {
+      const int64_t idx = team + step * p.stride;
+      bool approx = mode == kTafPredicting;
+      double outv;
+      if (approx) {
+        outv = lastv;
+        if (--rem == 0) {
+          cnt = 0;
+          head = 0;
+          mode = kTafFilling;
+        }
+      } else {
+        double o[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) o[d] = p.region.in[idx * 5 + d];
+        bool ok;
+        outv = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
+                   : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok);
+        if (!ok) err = true;
+        // TafState::observe_accurate (single output)
+        const int h = p.taf_h;
+        if (lane == 0) {
+          int slot;
+          if (cnt < h) {
+            slot = head + cnt;
+            if (slot >= h) slot -= h;
+          } else {
+            slot = head;
+          }
+          ring[slot] = outv;
+        }
+        __syncwarp();
+        if (cnt < h) ++cnt; else head = head + 1 == h ? 0 : head + 1;
+        lastv = outv;
+        if (mode == kTafPredicting) {
+          if (--rem == 0) {
+            cnt = 0;
+            head = 0;
+            mode = kTafFilling;
+          }
+        } else if ((mode == kTafFilling && cnt == h) || mode == kTafChecking) {
+          if (taf_ring_passes(ring, 1, h, head, cnt, p.taf_thr)) {
+            rem = p.taf_p;
+            mode = kTafPredicting;
+          } else {
+            mode = kTafChecking;
+          }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (p.region.out) p.region.out[idx] = outv;
+        if (p.paths) p.paths[idx] = approx ? 1 : 0;
+      }
+      tot += tpt;
+      wsteps += wpt;
+      if (approx) app += tpt;
+    }
+    if (lane != 0) tot = app = wsteps = 0;
+    flush_stats(p, tot, app, wsteps, (lane == 0 && trip > 0) ? wpt : 0ull, err);
+    return;
+  }
+
+  for (int64_t base = 0; base < trip; base += kBinoChunk) {
+    const int cnt = (int)(trip - base < kBinoChunk ? trip - base : kBinoChunk);
+    // ---- phase 1: decisions for the chunk (input-only; thread 0) ----------
+    if (threadIdx.x == 0) {
+      int nm = 0;
+      for (int s = 0; s < cnt; ++s) {
+        const int64_t step = base + s;
+        const int64_t idx = team + step * p.stride;
+        int a = kActMiss;
+        if (TECH == HPAC_TECH_IACT) {
+          double in[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) in[d] = p.region.in[idx * 5 + d];
+          int hit, near;
+          team_lookup(tab, 1, 5, 5, in, occ, p.iact_thr, hit, near);
+          if (hit >= 0) {
+            int src = slot_src[hit];
+            a = src >= base ? -(3 + (int)(src - base)) : hit;
+          } else {
+            // miss: the (lowest) lane inserts at the round-robin cursor
+#pragma unroll
+            for (int d = 0; d < 5; ++d) tab[rr * 5 + d] = in[d];
+            slot_src[rr] = (int)step;
+            rr = rr + 1 == p.tsize ? 0 : rr + 1;
+            occ = occ + 1 < p.tsize ? occ + 1 : p.tsize;
+          }
+        } else if (TECH == HPAC_TECH_PERFO) {
+          if (perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, step, trip,
+                                team))
+            a = kActSkip;
+        }
+        act[s] = a;
+        if (a == kActMiss) miss[nm++] = s;
+        tot += tpt;
+        wsteps += wpt;
+        if (a != kActMiss) app += tpt;
+        if (p.paths) p.paths[idx] = a != kActMiss ? 1 : 0;
+      }
+      *nmiss_s = nm;
+    }
+    __syncthreads();
+    // ---- phase 2: misses evaluated by the team's warps --------------------
+    const int nm = *nmiss_s;
+    for (int m = warp; m < nm; m += kBinoWarps) {
+      const int s = miss[m];
+      const int64_t idx = team + (base + s) * p.stride;
+      double o[5];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) o[d] = __ldg(p.region.in + idx * 5 + d);
+      bool ok;
+      double v = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
+                     : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok);
+      if (!ok) err = true;
+      if (lane == 0) price[s] = v;
+    }
+    __syncthreads();
+    // ---- phase 3: outputs (misses, hits from this or earlier chunks) -------
+    for (int s = threadIdx.x; s < cnt; s += blockDim.x) {
+      const int a = act[s];
+      if (a == kActSkip) continue;
+      double v;
+      if (a == kActMiss)
+        v = price[s];
+      else if (a >= 0)
+        v = slot_val[a];
+      else
+        v = price[-(a + 3)];
+      if (p.region.out) p.region.out[team + (base + s) * p.stride] = v;
+    }
+    __syncthreads();
+    // carry slot payloads produced in this chunk to the next one
+    if (TECH == HPAC_TECH_IACT && threadIdx.x == 0) {
+      for (int t = 0; t < occ; ++t)
+        if (slot_src[t] >= base) slot_val[t] = price[slot_src[t] - base];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) tot = app = wsteps = 0;
+  flush_stats(p, tot, app, wsteps, (threadIdx.x == 0 && trip > 0) ? wpt : 0ull, err);
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+// ---------------------------------------------------------------------------
+size_t binomial_team_smem(EngineParams& p) {
+  const int N = p.region.binomial_steps;
+  const bool big = N + 1 > 32 * kLatBmax;
+  const int ts = p.tsize > 0 ? p.tsize : 1;
+  size_t tabsz = 5 * (size_t)ts;
+  if (p.tech == HPAC_TECH_TAF && (size_t)p.taf_h > tabsz) tabsz = p.taf_h;  // TAF ring
+  p.smem_tab_off = kBinoChunk + ts;
+  p.smem_scratch_off = (int)(p.smem_tab_off + tabsz);
+  size_t dbl = p.smem_scratch_off + (size_t)kBinoWarps * (big ? 2 * (N + 2) : 32 * kLatBmax);
+  p.smem_ctl_off = (int)dbl;
+  size_t ints = 2 * kBinoChunk + ts + 2;
+  return dbl * sizeof(double) + ints * sizeof(int);
+}
+
+size_t engine_team_seq_smem(EngineParams& p, int block) {
+  size_t off = 0;
+  p.smem_taf_off = 0;
+  if (p.tech == HPAC_TECH_TAF && !(p.out_dims == 1 && p.taf_h <= 8)) {
+    off += (size_t)p.out_dims * p.taf_h * block;
+  }
+  p.smem_tab_off = (int)off;
+  if (p.tech == HPAC_TECH_IACT) off += (size_t)p.tsize * (p.in_dims + p.out_dims) * block;
+  p.smem_ctl_off = (int)off;
+  return off * sizeof(double) + 16;
+}
+
+template <class App, int TECH>
+static cudaError_t launch_seq(const EngineParams& p, int team_end, int block, size_t smem,
+                              cudaStream_t st) {
+  int nteams = team_end - p.team_begin;
+  int grid = (nteams + block - 1) / block;
+  int hreg = (TECH == HPAC_TECH_TAF && p.out_dims == 1 && p.taf_h <= 8) ? p.taf_h : 0;
+#define HPAC_SEQ(H)                                                                         \
+  {                                                                                         \
+    auto k = engine_team_seq_kernel<App, TECH, H>;                                          \
+    if (smem > 48 * 1024) {                                                                 \
+      cudaError_t e =                                                                       \
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+      if (e != cudaSuccess) return e;                                                       \
+    }                                                                                       \
+    k<<<grid, block, smem, st>>>(p, team_end);                                              \
+    return cudaGetLastError();                                                              \
+  }
+  if (TECH == HPAC_TECH_TAF) {
+    switch (hreg) {
+      case 1: HPAC_SEQ(1);
+      case 2: HPAC_SEQ(2);
+      case 3: HPAC_SEQ(3);
+      case 4: HPAC_SEQ(4);
+      case 5: HPAC_SEQ(5);
+      case 6: HPAC_SEQ(6);
+      case 7: HPAC_SEQ(7);
+      case 8: HPAC_SEQ(8);
+      default: HPAC_SEQ(0);
+    }
+  }
+  HPAC_SEQ(0);
+#undef HPAC_SEQ
+}
+
+template <class App>
+static cudaError_t launch_seq_app(const EngineParams& p, int team_end, int block, size_t smem,
+                                  cudaStream_t st) {
+  switch (p.tech) {
+    case HPAC_TECH_TAF: return launch_seq<App, HPAC_TECH_TAF>(p, team_end, block, smem, st);
+    case HPAC_TECH_IACT: return launch_seq<App, HPAC_TECH_IACT>(p, team_end, block, smem, st);
+    case HPAC_TECH_PERFO: return launch_seq<App, HPAC_TECH_PERFO>(p, team_end, block, smem, st);
+    default: return launch_seq<App, kTechNoneT>(p, team_end, block, smem, st);
+  }
+}
+
+cudaError_t engine_team_seq_launch(const EngineParams& p, int team_end, int block, size_t smem,
+                                   cudaStream_t st) {
+  switch (p.region.app) {
+    case HPAC_APP_TABLE: return launch_seq_app<AppTable>(p, team_end, block, smem, st);
+    case HPAC_APP_SYNTHETIC: return launch_seq_app<AppSynthetic>(p, team_end, block, smem, st);
+    case HPAC_APP_BLACKSCHOLES:
+      return launch_seq_app<AppBlackScholes>(p, team_end, block, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int TECH, bool AM, bool PUT>
+static cudaError_t launch_bino3(const EngineParams& p, int nblocks, size_t smem,
+                                cudaStream_t st) {
+  auto k = binomial_team_kernel<TECH, AM, PUT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<nblocks, kBinoWarps * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int TECH>
+static cudaError_t launch_bino2(const EngineParams& p, int nblocks, size_t smem,
+                                cudaStream_t st) {
+  const bool am = p.region.binomial_american != 0, put = p.region.binomial_put != 0;
+  if (am && put) return launch_bino3<TECH, true, true>(p, nblocks, smem, st);
+  if (am && !put) return launch_bino3<TECH, true, false>(p, nblocks, smem, st);
+  if (!am && put) return launch_bino3<TECH, false, true>(p, nblocks, smem, st);
+  return launch_bino3<TECH, false, false>(p, nblocks, smem, st);
+}
+
+cudaError_t binomial_team_launch(const EngineParams& p, int nblocks, size_t smem,
+                                 cudaStream_t st) {
+  switch (p.tech) {
+    case HPAC_TECH_TAF: return launch_bino2<HPAC_TECH_TAF>(p, nblocks, smem, st);
+    case HPAC_TECH_IACT: return launch_bino2<HPAC_TECH_IACT>(p, nblocks, smem, st);
+    case HPAC_TECH_PERFO: return launch_bino2<HPAC_TECH_PERFO>(p, nblocks, smem, st);
+    default: return launch_bino2<kTechNoneT>(p, nblocks, smem, st);
+  }
+}
+
+}  // namespace hpac

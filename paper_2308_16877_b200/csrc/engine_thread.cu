@@ -1,0 +1,531 @@
+// engine_thread.cu — the approximate-region engine for the per-thread work
+// mapping (WorkMapping::kPerThread, grid.hpp:14), i.e. run_region
+// (engine.hpp:132-402) for regions whose threads own distinct work items.
+//
+// Mapping onto the hardware: one CTA = one logical team; one CUDA thread =
+// one logical thread; a logical warp of `ws` lanes is a lane segment of a
+// hardware warp when ws divides 32 (votes = __ballot_sync + __popc on the
+// segment, iACT writer = shuffle butterfly), otherwise a shared-memory
+// group (generic path). Per-thread technique state lives in registers
+// (TAF window as a shift register for h <= 8, perforation counters) and
+// per-warp iACT tables live in shared memory. The grid-stride schedule is
+// the reference's: item = tid + step * G with G = num_teams * tpt, so each
+// thread's decision stream is identical to the reference's.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "apps.cuh"
+#include "engine.h"
+#include "hpac_device.cuh"
+
+namespace hpac {
+
+constexpr int kTechNone = 3;
+
+namespace {
+
+// Triple-buffered shared counters: one __syncthreads per use.
+struct CtlLayout {
+  // ints
+  static constexpr int kTeamYes = 0;   // [3]
+  static constexpr int kTeamAct = 3;   // [3]
+  static constexpr int kBarMax = 6;    // [3] barrier-divergence max arrivals
+  static constexpr int kBarMiss = 9;   // [3]
+  static constexpr int kGeneric = 16;  // generic-ws per-logical-warp words start here
+};
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v, unsigned mask) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+}  // namespace
+
+template <class App, int TECH, int HREG, int MAXT>
+__global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams p) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int IN_MAX = App::IN_MAX;
+  constexpr int OUT_MAX = App::OUT_MAX;
+
+  const int local = threadIdx.x;
+  const int team = p.team_begin + (int)blockIdx.x;
+  const int64_t tid = (int64_t)team * p.tpt + local;
+  const int ws = p.ws;
+  const int lane = local % ws;   // logical lane
+  const int wloc = local / ws;   // logical warp within the team
+  const int hw_lane = local & 31;
+  const int hw_warp = local >> 5;
+  const int hw_count = min(32, p.tpt - hw_warp * 32);
+  const unsigned hw_mask = hw_count == 32 ? 0xffffffffu : ((1u << hw_count) - 1u);
+  const bool fast = p.fast_ws != 0;
+  const int seg_base = hw_lane - lane;  // fast path only
+  const unsigned seg_mask = ws >= 32 ? 0xffffffffu : (((1u << ws) - 1u) << seg_base);
+  int* ctl = reinterpret_cast<int*>(smem + p.smem_ctl_off);
+  int* gw = ctl + CtlLayout::kGeneric;  // generic-ws words: [wpt][4] + tables [T][3]
+  for (int i = local; i < p.ctl_ints; i += blockDim.x) ctl[i] = 0;
+  App::init(p, smem + p.smem_scratch_off);
+  __syncthreads();
+
+  // ---- TAF state (TafState, taf.hpp:59-163) -------------------------------
+  int taf_mode = kTafFilling, taf_rem = 0, taf_count = 0, taf_head = 0;
+  double win[HREG > 0 ? HREG : 1];
+  double last[OUT_MAX];
+#pragma unroll
+  for (int d = 0; d < OUT_MAX; ++d) last[d] = 0.0;
+#pragma unroll
+  for (int i = 0; i < (HREG > 0 ? HREG : 1); ++i) win[i] = 0.0;
+  double* ring = smem + p.smem_taf_off;  // [d][slot][tpt] (smem variant)
+
+  // ---- iACT per-table bookkeeping (MemoTable, iact.hpp:58-145) -----------
+  const int tpw = TECH == HPAC_TECH_IACT ? p.tpw : 1;
+  const int group = ws / tpw;                       // lanes sharing one table
+  const int T = p.wpt * tpw;                        // tables in this team
+  const int tab = wloc * tpw + lane / group;        // this lane's table
+  const int D = p.in_dims + p.out_dims;
+  double* tabs = smem + p.smem_tab_off;             // [(slot*D + c) * T + tab]
+  int rr = 0, occ = 0;
+
+  // ---- perforation counters (engine.hpp:70-71) -----------------------------
+  int64_t pcount = 0, hcount = 0;
+  int64_t trip = 0;
+  if (TECH == HPAC_TECH_PERFO &&
+      (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
+    trip = trip_count(tid, p.stride, p.n, p.steps);
+
+  // ---- stats ---------------------------------------------------------------
+  unsigned long long s_total = 0, s_approx = 0, s_warp = 0, s_div = 0;
+  bool touched = false;
+  bool app_error = false;
+  int round_ctr = 0;  // global round counter for triple buffers
+
+  for (int64_t step = 0; step < p.steps; ++step) {
+    const int64_t idx = tid + step * p.stride;
+    const bool active = idx < p.n;
+    int enc = 1;
+    if (p.has_enc && active) enc = p.region.encounters[idx];
+    int rounds = 1;
+    if (p.has_enc) {
+      // team max of encounters (engine.hpp:194-215); block-uniform
+      __shared__ int s_rounds[2];
+      if (local == 0) s_rounds[step & 1] = 0;
+      __syncthreads();
+      if (active) atomicMax(&s_rounds[step & 1], enc);
+      __syncthreads();
+      rounds = s_rounds[step & 1];
+    }
+    int arrivals = 0;
+    uint8_t pbits = 0;
+
+    for (int round = 0; round < rounds; ++round, ++round_ctr) {
+      const int buf = round_ctr % 3;
+      const bool in_round = active && round < enc;
+
+      // ---- predicate phase (engine.hpp:221-251) ----------------------------
+      double in[IN_MAX];
+      bool loaded = false;
+      bool pred = false;
+      int hit = -1, near = -1;
+      double min_d = dinf();
+      if (in_round) {
+        if (TECH == HPAC_TECH_TAF) {
+          pred = taf_mode == kTafPredicting;
+        } else if (TECH == HPAC_TECH_IACT) {
+          App::load(p, idx, in);
+          loaded = true;
+          // MemoTable::lookup / min_distance / nearest_slot in one scan
+          double hit_d = 0.0, near_d = dinf();
+          for (int s = 0; s < occ; ++s) {
+            double ssq = 0.0;
+#pragma unroll
+            for (int c = 0; c < IN_MAX; ++c)
+              if (c < p.in_dims) {
+                double df = __dsub_rn(tabs[(s * D + c) * T + tab], in[c]);
+                ssq = __dadd_rn(ssq, __dmul_rn(df, df));
+              }
+            double dd = __dsqrt_rn(ssq);
+            if (dd <= p.iact_thr && (hit < 0 || dd < hit_d)) {
+              hit = s;
+              hit_d = dd;
+            }
+            if (dd < near_d) {
+              near_d = dd;
+              near = s;
+            }
+          }
+          min_d = near_d;
+          pred = hit >= 0;
+        } else if (TECH == HPAC_TECH_PERFO) {
+          const bool herded = p.perfo_kind == HPAC_PERFO_HERDED_SMALL ||
+                              p.perfo_kind == HPAC_PERFO_HERDED_LARGE;
+          pred = perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed,
+                                   herded ? hcount : pcount, trip, tid);
+        }
+      }
+
+      // ---- decision hierarchy (hierarchy.hpp:33-70, engine.hpp:257-298) ----
+      bool approx = pred;
+      bool team_any = true;
+      if (TECH != kTechNone && p.voting) {
+        if (p.level == HPAC_LEVEL_TEAM) {
+          int* yes = ctl + CtlLayout::kTeamYes;
+          int* act = ctl + CtlLayout::kTeamAct;
+          if (local == 0) {
+            yes[(buf + 1) % 3] = 0;
+            act[(buf + 1) % 3] = 0;
+          }
+          unsigned bv = __ballot_sync(hw_mask, in_round && pred);
+          unsigned ba = __ballot_sync(hw_mask, in_round);
+          if (hw_lane == 0 && ba) {
+            atomicAdd(&yes[buf], __popc(bv));
+            atomicAdd(&act[buf], __popc(ba));
+          }
+          __syncthreads();
+          int ty = yes[buf], ta = act[buf];
+          team_any = ta > 0;
+          approx = 2 * ty > ta;  // majority_decision, hierarchy.hpp:33-35
+          if (active && team_any) arrivals += 1;  // the vote's framework barrier
+        } else if (fast) {
+          unsigned bv = __ballot_sync(hw_mask, in_round && pred) & seg_mask;
+          unsigned ba = __ballot_sync(hw_mask, in_round) & seg_mask;
+          approx = 2 * __popc(bv) > __popc(ba);
+        } else {
+          int* w = gw + wloc * 4;
+          __syncthreads();
+          if (lane == 0) {
+            w[0] = 0;
+            w[1] = 0;
+          }
+          __syncthreads();
+          if (in_round) {
+            atomicAdd(&w[1], 1);
+            if (pred) atomicAdd(&w[0], 1);
+          }
+          __syncthreads();
+          approx = 2 * w[0] > w[1];
+        }
+      }
+
+      // ---- lane execution (engine.hpp:303-347) -----------------------------
+      double out[OUT_MAX];
+#pragma unroll
+      for (int d = 0; d < OUT_MAX; ++d) out[d] = 0.0;
+      bool cand = false;
+      if (in_round) {
+        if (approx) {
+          if (TECH == HPAC_TECH_TAF) {
+            // TafState::emit_approx, taf.hpp:114-117
+#pragma unroll
+            for (int d = 0; d < OUT_MAX; ++d) out[d] = last[d];
+            if (taf_mode == kTafPredicting && --taf_rem == 0) {
+              taf_count = 0;
+              taf_head = 0;
+              taf_mode = kTafFilling;
+            }
+            App::store(p, idx, out);
+          } else if (TECH == HPAC_TECH_IACT) {
+            int slot = hit >= 0 ? hit : (occ > 0 ? near : -1);
+            if (slot >= 0) {
+#pragma unroll
+              for (int d = 0; d < OUT_MAX; ++d)
+                if (d < p.out_dims) out[d] = tabs[(slot * D + p.in_dims + d) * T + tab];
+              App::store(p, idx, out);
+            } else {
+              approx = false;  // empty table: accurate fallback (engine.hpp:327-331)
+            }
+          }
+          // perforation: output untouched
+        }
+        if (!approx) {
+          if (!loaded) App::load(p, idx, in);
+          if (!App::eval(p, idx, in, out, smem + p.smem_scratch_off)) app_error = true;
+          if (p.barrier_eval) arrivals += 1;
+          App::store(p, idx, out);
+          if (TECH == HPAC_TECH_TAF) {
+            // TafState::observe_accurate, taf.hpp:94-108
+            bool full;
+            if (HREG > 0) {
+#pragma unroll
+              for (int i = 0; i + 1 < (HREG > 0 ? HREG : 1); ++i) win[i] = win[i + 1];
+              win[(HREG > 0 ? HREG : 1) - 1] = out[0];
+              if (taf_count < HREG) ++taf_count;
+              full = taf_count == HREG;
+            } else {
+              const int h = p.taf_h;
+              int slot;
+              if (taf_count < h) {
+                slot = taf_head + taf_count;
+                if (slot >= h) slot -= h;
+                ++taf_count;
+              } else {
+                slot = taf_head;
+                taf_head = taf_head + 1 == h ? 0 : taf_head + 1;
+              }
+              for (int d = 0; d < p.out_dims; ++d)
+                ring[(d * h + slot) * p.tpt + local] = out[d];
+              full = taf_count == h;
+            }
+#pragma unroll
+            for (int d = 0; d < OUT_MAX; ++d) last[d] = out[d];
+            bool check = (taf_mode == kTafFilling && full) || taf_mode == kTafChecking;
+            if (taf_mode == kTafPredicting) {
+              if (--taf_rem == 0) {
+                taf_count = 0;
+                taf_head = 0;
+                taf_mode = kTafFilling;
+              }
+            } else if (check) {
+              bool pass;
+              if (HREG > 0) {
+                pass = taf_window_passes<(HREG > 0 ? HREG : 1)>(win, p.taf_thr);
+              } else {
+                pass = true;
+                for (int d = 0; d < p.out_dims && pass; ++d)
+                  pass = taf_ring_passes(ring + d * p.taf_h * p.tpt + local, p.tpt, p.taf_h,
+                                         taf_head, taf_count, p.taf_thr);
+              }
+              if (pass) {
+                taf_rem = p.taf_p;
+                taf_mode = kTafPredicting;
+              } else {
+                taf_mode = kTafChecking;
+              }
+            }
+          }
+          if (TECH == HPAC_TECH_IACT && hit < 0) cand = true;
+        }
+        s_total += 1;
+        if (approx) {
+          s_approx += 1;
+          if (round < 8) pbits |= (uint8_t)(1u << round);
+        }
+      }
+
+      // ---- iACT write phase (engine.hpp:351-366, iact.hpp:166-180) ----------
+      if (TECH == HPAC_TECH_IACT) {
+        double bd = cand ? min_d : -1.0;
+        int bl = lane;
+        if (fast) {
+          for (int off = group >> 1; off > 0; off >>= 1) {
+            double od = __shfl_xor_sync(hw_mask, bd, off);
+            int ol = __shfl_xor_sync(hw_mask, bl, off);
+            if (writer_better(od, ol, bd, bl)) {
+              bd = od;
+              bl = ol;
+            }
+          }
+          __syncwarp(hw_mask);
+        } else {
+          unsigned long long* tk = reinterpret_cast<unsigned long long*>(gw + p.wpt * 4);
+          int* tl = gw + p.wpt * 4 + 2 * T;
+          __syncthreads();
+          if (lane % group == 0) {
+            tk[tab] = 0ull;
+            tl[tab] = 1 << 30;
+          }
+          __syncthreads();
+          // candidate keys: +1 so that a real distance 0 beats "no candidate"
+          unsigned long long key =
+              cand ? (unsigned long long)__double_as_longlong(min_d) + 1ull : 0ull;
+          if (cand) atomicMax(&tk[tab], key);
+          __syncthreads();
+          if (cand && key == tk[tab]) atomicMin(&tl[tab], lane);
+          __syncthreads();
+          bd = tk[tab] ? 0.0 : -1.0;
+          bl = tl[tab];
+        }
+        if (bd >= 0.0) {
+          if (lane == bl) {
+            // MemoTable::insert at the round-robin cursor, iact.hpp:124-135
+#pragma unroll
+            for (int c = 0; c < IN_MAX; ++c)
+              if (c < p.in_dims) tabs[(rr * D + c) * T + tab] = in[c];
+#pragma unroll
+            for (int d = 0; d < OUT_MAX; ++d)
+              if (d < p.out_dims) tabs[(rr * D + p.in_dims + d) * T + tab] = out[d];
+          }
+          rr = rr + 1 == p.tsize ? 0 : rr + 1;
+          occ = occ + 1 < p.tsize ? occ + 1 : p.tsize;
+        }
+        if (fast)
+          __syncwarp(hw_mask);
+        else
+          __syncthreads();
+      }
+
+      // ---- perforation counters + warp stats (engine.hpp:368-378) -----------
+      bool any_lw, mixed;
+      if (fast) {
+        unsigned ba = __ballot_sync(hw_mask, in_round) & seg_mask;
+        unsigned bx = __ballot_sync(hw_mask, in_round && approx) & seg_mask;
+        any_lw = ba != 0;
+        mixed = bx != 0 && bx != ba;
+      } else {
+        int* w = gw + wloc * 4;
+        __syncthreads();
+        if (lane == 0) {
+          w[2] = 0;
+          w[3] = 0;
+        }
+        __syncthreads();
+        if (in_round) atomicAdd(&w[approx ? 3 : 2], 1);
+        __syncthreads();
+        any_lw = (w[2] + w[3]) > 0;
+        mixed = w[2] > 0 && w[3] > 0;
+      }
+      if (TECH == HPAC_TECH_PERFO) {
+        if (in_round) pcount += 1;
+        if (any_lw) hcount += 1;
+      }
+      if (lane == 0 && any_lw) {
+        touched = true;
+        s_warp += 1;
+        if (mixed) s_div += 1;
+      }
+      (void)team_any;
+    }
+
+    if (p.paths && active) p.paths[idx] = pbits;
+
+    // ---- TeamState::end_step barrier check (machine.hpp:53-61) -------------
+    if (p.barrier_eval) {
+      const int b = step % 3;
+      int* bmax = ctl + CtlLayout::kBarMax;
+      int* bmiss = ctl + CtlLayout::kBarMiss;
+      if (local == 0) {
+        bmax[(b + 1) % 3] = 0;
+        bmiss[(b + 1) % 3] = 0;
+      }
+      __syncthreads();
+      if (active) atomicMax(&bmax[b], arrivals);
+      __syncthreads();
+      if (active && arrivals < bmax[b]) atomicAdd(&bmiss[b], 1);
+      __syncthreads();
+      if (local == 0 && bmiss[b] > 0) {
+        unsigned long long key = ((unsigned long long)step << 32) | (unsigned)team;
+        unsigned long long prev = atomicMin(&p.counters[kCntBarrierKey], key);
+        if (key < prev) atomicExch(&p.counters[kCntBarrierMissing], (unsigned long long)bmiss[b]);
+      }
+    }
+  }
+
+  // ---- reduce stats: one atomic per hardware warp per counter -----------------
+  s_total = warp_sum_u64(s_total, hw_mask);
+  s_approx = warp_sum_u64(s_approx, hw_mask);
+  s_warp = warp_sum_u64(s_warp, hw_mask);
+  s_div = warp_sum_u64(s_div, hw_mask);
+  unsigned long long s_res = warp_sum_u64((lane == 0 && touched) ? 1ull : 0ull, hw_mask);
+  unsigned any_err = __ballot_sync(hw_mask, app_error);
+  if (hw_lane == 0) {
+    if (s_total) atomicAdd(&p.counters[kCntTotal], s_total);
+    if (s_approx) atomicAdd(&p.counters[kCntApprox], s_approx);
+    if (s_div) atomicAdd(&p.counters[kCntDivergent], s_div);
+    if (s_warp) atomicAdd(&p.counters[kCntWarpSteps], s_warp);
+    if (s_res) atomicAdd(&p.counters[kCntResidentWarps], s_res);
+    if (any_err) atomicAdd(&p.counters[kCntAppError], 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+// ---------------------------------------------------------------------------
+template <class App, int TECH>
+static cudaError_t launch_tech(const EngineParams& p, int nblocks, size_t smem,
+                               cudaStream_t st) {
+  // TAF: register shift-register window for single-output regions, h <= 8
+  int hreg = 0;
+  if (TECH == HPAC_TECH_TAF && p.out_dims == 1 && p.taf_h <= 8) hreg = p.taf_h;
+#define HPAC_LAUNCH(H)                                                                  \
+  {                                                                                     \
+    auto k = p.tpt <= 256 ? engine_thread_kernel<App, TECH, H, 256>                     \
+                          : engine_thread_kernel<App, TECH, H, 1024>;                   \
+    if (smem > 48 * 1024) {                                                             \
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)smem);                                  \
+      if (e != cudaSuccess) return e;                                                   \
+    }                                                                                   \
+    k<<<nblocks, p.tpt, smem, st>>>(p);                                                 \
+    return cudaGetLastError();                                                          \
+  }
+  if (TECH == HPAC_TECH_TAF) {
+    switch (hreg) {
+      case 1: HPAC_LAUNCH(1);
+      case 2: HPAC_LAUNCH(2);
+      case 3: HPAC_LAUNCH(3);
+      case 4: HPAC_LAUNCH(4);
+      case 5: HPAC_LAUNCH(5);
+      case 6: HPAC_LAUNCH(6);
+      case 7: HPAC_LAUNCH(7);
+      case 8: HPAC_LAUNCH(8);
+      default: HPAC_LAUNCH(0);
+    }
+  }
+  HPAC_LAUNCH(0);
+#undef HPAC_LAUNCH
+}
+
+template <class App>
+static cudaError_t launch_app(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st) {
+  switch (p.tech) {
+    case HPAC_TECH_TAF: return launch_tech<App, HPAC_TECH_TAF>(p, nblocks, smem, st);
+    case HPAC_TECH_IACT: return launch_tech<App, HPAC_TECH_IACT>(p, nblocks, smem, st);
+    case HPAC_TECH_PERFO: return launch_tech<App, HPAC_TECH_PERFO>(p, nblocks, smem, st);
+    default: return launch_tech<App, kTechNone>(p, nblocks, smem, st);
+  }
+}
+
+// Dynamic shared memory for the per-thread engine; fills the offsets.
+size_t engine_thread_smem(EngineParams& p) {
+  size_t off = 0;  // in doubles
+  p.smem_taf_off = 0;
+  p.smem_last_off = 0;
+  if (p.tech == HPAC_TECH_TAF && !(p.out_dims == 1 && p.taf_h <= 8)) {
+    p.smem_taf_off = (int)off;
+    off += (size_t)p.out_dims * p.taf_h * p.tpt;
+  }
+  p.smem_tab_off = (int)off;
+  if (p.tech == HPAC_TECH_IACT)
+    off += (size_t)p.tsize * (p.in_dims + p.out_dims) * p.wpt * p.tpw;
+  p.smem_scratch_off = (int)off;
+  if (p.region.app == HPAC_APP_KMEANS)
+    off += (size_t)p.region.kmeans_k * p.region.kmeans_dims;
+  p.smem_ctl_off = (int)off;
+  // control ints: 16 fixed + generic-ws words (4 per logical warp + 3 per table)
+  size_t ctl_ints = 16 + 4 * (size_t)p.wpt + 3 * (size_t)p.wpt * (p.tpw > 0 ? p.tpw : 1) + 4;
+  p.ctl_ints = (int)ctl_ints;
+  off += (ctl_ints + 1) / 2 + 1;
+  return off * sizeof(double);
+}
+
+int engine_thread_max_in(int app) {
+  switch (app) {
+    case HPAC_APP_TABLE: return AppTable::IN_MAX;
+    case HPAC_APP_SYNTHETIC: return AppSynthetic::IN_MAX;
+    case HPAC_APP_BLACKSCHOLES: return AppBlackScholes::IN_MAX;
+    case HPAC_APP_KMEANS: return AppKmeans::IN_MAX;
+  }
+  return 0;
+}
+int engine_thread_max_out(int app) {
+  switch (app) {
+    case HPAC_APP_TABLE: return AppTable::OUT_MAX;
+    case HPAC_APP_SYNTHETIC: return AppSynthetic::OUT_MAX;
+    case HPAC_APP_BLACKSCHOLES: return AppBlackScholes::OUT_MAX;
+    case HPAC_APP_KMEANS: return AppKmeans::OUT_MAX;
+  }
+  return 0;
+}
+
+cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem,
+                                 cudaStream_t st) {
+  switch (p.region.app) {
+    case HPAC_APP_TABLE: return launch_app<AppTable>(p, nblocks, smem, st);
+    case HPAC_APP_SYNTHETIC: return launch_app<AppSynthetic>(p, nblocks, smem, st);
+    case HPAC_APP_BLACKSCHOLES: return launch_app<AppBlackScholes>(p, nblocks, smem, st);
+    case HPAC_APP_KMEANS: return launch_app<AppKmeans>(p, nblocks, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hpac

@@ -1,0 +1,659 @@
+// runtime.cu — host side of the C-ABI (include/hpac_offload.h): validation
+// with the reference's error taxonomy, arena accounting, grid resolution,
+// kernel dispatch, statistics, host-buffer (end-to-end) entry, metrics.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "hpac_offload.h"
+
+#define HPAC_API extern "C" __attribute__((visibility("default")))
+
+namespace hpac {
+size_t engine_thread_smem(EngineParams& p);
+int engine_thread_max_in(int app);
+int engine_thread_max_out(int app);
+cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st);
+size_t engine_team_seq_smem(EngineParams& p, int block);
+cudaError_t engine_team_seq_launch(const EngineParams& p, int team_end, int block, size_t smem,
+                                   cudaStream_t st);
+size_t binomial_team_smem(EngineParams& p);
+cudaError_t binomial_team_launch(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st);
+cudaError_t mape_launch(const double* a, const double* b, int64_t n, double* d_sum,
+                        unsigned long long* d_inf, cudaStream_t st);
+cudaError_t mcr_launch(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* d_cnt,
+                       cudaStream_t st);
+}  // namespace hpac
+
+using namespace hpac;
+
+namespace {
+
+int fail(char* err, size_t len, int code, const char* fmt, ...) {
+  if (err && len) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, len, fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+int cuda_fail(char* err, size_t len, cudaError_t e, const char* where) {
+  return fail(err, len, HPAC_ERR_CUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
+}
+
+// Per-host-thread launch scratch: device counters + pinned readback + events.
+struct Scratch {
+  int device = -1;
+  unsigned long long* d_cnt = nullptr;
+  unsigned long long* h_cnt = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  hpac_stats_t last{};
+  bool pending = false;
+  cudaStream_t pending_stream = nullptr;
+  hpac_stats_t pending_base{};
+};
+thread_local Scratch g_scratch;
+
+cudaError_t scratch_ready() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_scratch.device == dev && g_scratch.d_cnt) return cudaSuccess;
+  if ((e = cudaMalloc(&g_scratch.d_cnt, sizeof(unsigned long long) * kNumCounters)) != cudaSuccess)
+    return e;
+  if ((e = cudaMallocHost(&g_scratch.h_cnt, sizeof(unsigned long long) * kNumCounters)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaEventCreate(&g_scratch.ev0)) != cudaSuccess) return e;
+  if ((e = cudaEventCreate(&g_scratch.ev1)) != cudaSuccess) return e;
+  g_scratch.device = dev;
+  return cudaSuccess;
+}
+
+bool kind_uses_modulus(int k) {
+  return k == HPAC_PERFO_SMALL || k == HPAC_PERFO_LARGE || k == HPAC_PERFO_HERDED_SMALL ||
+         k == HPAC_PERFO_HERDED_LARGE;
+}
+
+// grid.hpp:27-37
+int validate_grid(const hpac_grid_t* g, char* err, size_t el) {
+  if (!g) return fail(err, el, HPAC_ERR_CONFIG, "grid is null");
+  if (g->num_teams < 1) return fail(err, el, HPAC_ERR_CONFIG, "num_teams must be positive");
+  if (g->threads_per_team < 1)
+    return fail(err, el, HPAC_ERR_CONFIG, "threads_per_team must be positive");
+  if (g->warp_size < 1 || g->warp_size > 64)
+    return fail(err, el, HPAC_ERR_CONFIG, "warp_size must be in [1, 64]");
+  if (g->threads_per_team % g->warp_size != 0)
+    return fail(err, el, HPAC_ERR_CONFIG, "warp_size (%d) must divide threads_per_team (%d)",
+                g->warp_size, g->threads_per_team);
+  if (g->items_per_thread < 1)
+    return fail(err, el, HPAC_ERR_CONFIG, "items_per_thread must be positive");
+  return 0;
+}
+
+// ApproxSpec::validate + Taf/Iact/PerfoConfig::validate (directive.hpp:72-84,
+// taf.hpp:19-23, iact.hpp:24-29, perfo.hpp:27-34)
+int validate_spec(const hpac_spec_t* s, char* err, size_t el) {
+  switch (s->technique) {
+    case HPAC_TECH_TAF:
+      if (s->taf_h_size < 1) return fail(err, el, HPAC_ERR_CONFIG, "TAF history size must be >= 1");
+      if (s->taf_p_size < 1)
+        return fail(err, el, HPAC_ERR_CONFIG, "TAF prediction size must be >= 1");
+      if (!(s->taf_threshold >= 0.0))
+        return fail(err, el, HPAC_ERR_CONFIG, "TAF threshold must be >= 0");
+      break;
+    case HPAC_TECH_IACT:
+      if (s->iact_table_size < 1)
+        return fail(err, el, HPAC_ERR_CONFIG, "iACT table size must be >= 1");
+      if (!(s->iact_threshold >= 0.0))
+        return fail(err, el, HPAC_ERR_CONFIG, "iACT threshold must be >= 0");
+      if (s->iact_tables_per_warp < 0)
+        return fail(err, el, HPAC_ERR_CONFIG, "tables_per_warp must be >= 1");
+      break;
+    case HPAC_TECH_PERFO:
+      if (s->perfo_kind < 0 || s->perfo_kind > HPAC_PERFO_RANDOM)
+        return fail(err, el, HPAC_ERR_CONFIG, "unknown perforation kind");
+      if (kind_uses_modulus(s->perfo_kind)) {
+        if (s->perfo_modulus < 2)
+          return fail(err, el, HPAC_ERR_CONFIG, "perforation modulus must be >= 2");
+      } else if (s->perfo_skip_percent < 1 || s->perfo_skip_percent > 99) {
+        return fail(err, el, HPAC_ERR_CONFIG, "perforation skip percent must be in [1, 99]");
+      }
+      break;
+    default:
+      return fail(err, el, HPAC_ERR_CONFIG, "ApproxSpec must carry exactly one technique payload");
+  }
+  if (s->level < HPAC_LEVEL_THREAD || s->level > HPAC_LEVEL_TEAM)
+    return fail(err, el, HPAC_ERR_CONFIG, "unknown decision level");
+  if (s->technique == HPAC_TECH_IACT && s->n_input_sections < 1)
+    return fail(err, el, HPAC_ERR_CONFIG, "iACT requires at least one input section");
+  if ((s->technique == HPAC_TECH_IACT || s->technique == HPAC_TECH_TAF) &&
+      s->n_output_sections < 1)
+    return fail(err, el, HPAC_ERR_CONFIG, "memoization requires at least one output section");
+  return 0;
+}
+
+// Region dims from the app (engine.hpp:26-33 input_dims/output_dims).
+int bind_region(hpac_region_t* r, char* err, size_t el) {
+  switch (r->app) {
+    case HPAC_APP_TABLE:
+      if (!r->table_out) return fail(err, el, HPAC_ERR_CONFIG, "region has no evaluate function");
+      if (r->input_dims > 0 && !r->in)
+        return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
+      if (r->output_dims < 1)
+        return fail(err, el, HPAC_ERR_CONFIG, "region output_dims must be >= 1");
+      if (r->input_dims < 0) return fail(err, el, HPAC_ERR_CONFIG, "region input_dims must be >= 0");
+      return 0;
+    case HPAC_APP_SYNTHETIC:
+      if (r->synthetic_profile < 0 || r->synthetic_profile > 2)
+        return fail(err, el, HPAC_ERR_CONFIG, "unknown synthetic profile");
+      r->input_dims = 1;
+      r->output_dims = 1;
+      return 0;
+    case HPAC_APP_BLACKSCHOLES:
+      r->input_dims = 5;
+      r->output_dims = 1;
+      if (!r->in) return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
+      return 0;
+    case HPAC_APP_BINOMIAL:
+      r->input_dims = 5;
+      r->output_dims = 1;
+      if (!r->in) return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
+      if (r->binomial_steps < 1)
+        return fail(err, el, HPAC_ERR_CONFIG, "binomial_price: n_steps must be >= 1");
+      return 0;
+    case HPAC_APP_KMEANS:
+      if (r->kmeans_dims < 1 || r->kmeans_k < 1)
+        return fail(err, el, HPAC_ERR_CONFIG, "kmeans dims and k must be >= 1");
+      if (!r->in || !r->centroids)
+        return fail(err, el, HPAC_ERR_CONFIG, "kmeans region needs points and centroids");
+      r->input_dims = r->kmeans_dims;
+      r->output_dims = r->kmeans_k;
+      return 0;
+  }
+  return fail(err, el, HPAC_ERR_UNSUPPORTED, "unsupported application id %d", r->app);
+}
+
+uint64_t taf_state_bytes(int h, int dims) { return (uint64_t)dims * (uint64_t)h * 8u + 16u; }
+uint64_t table_group_bytes(int tpw, int tsize, int in_dims, int out_dims) {
+  return (uint64_t)tpw * (uint64_t)tsize * (uint64_t)(in_dims + out_dims) * 8u +
+         (uint64_t)tpw * 2u * 4u;
+}
+
+// bind_technique arena charges (engine.hpp:83-116): the per-team bump
+// allocator fails at the first allocation that crosses the budget,
+// reporting required = used + length (arena.hpp:37-38).
+int arena_account(const hpac_grid_t* g, const hpac_region_t* r, const hpac_spec_t* s, int tpw,
+                  uint64_t* required, uint64_t* available, char* err, size_t el) {
+  const uint64_t cap = g->shared_mem_budget_bytes;
+  uint64_t used = 0, per = 0;
+  int count = 0;
+  *available = cap;
+  if (s->technique == HPAC_TECH_TAF) {
+    per = taf_state_bytes(s->taf_h_size, r->output_dims);
+    count = g->threads_per_team;
+  } else if (s->technique == HPAC_TECH_IACT) {
+    per = table_group_bytes(tpw, s->iact_table_size, r->input_dims, r->output_dims);
+    count = g->threads_per_team / g->warp_size;
+  }
+  if (count > 0 && per > 0) {
+    uint64_t fit = cap / per;  // allocations that fit
+    if (fit < (uint64_t)count) {
+      *required = (fit + 1) * per;
+      return fail(err, el, HPAC_ERR_ARENA_OVERFLOW,
+                  "shared arena overflow: required %llu bytes, available %llu bytes",
+                  (unsigned long long)*required, (unsigned long long)cap);
+    }
+    used = per * (uint64_t)count;
+  }
+  if (s->level == HPAC_LEVEL_TEAM) {
+    if (used + 8 > cap) {
+      *required = used + 8;
+      return fail(err, el, HPAC_ERR_ARENA_OVERFLOW,
+                  "shared arena overflow: required %llu bytes, available %llu bytes",
+                  (unsigned long long)*required, (unsigned long long)cap);
+    }
+    used += 8;
+  }
+  *required = used;
+  return 0;
+}
+
+struct Prepared {
+  EngineParams p{};
+  int kind = 0;  // 0 = per-thread engine, 1 = team seq, 2 = binomial team
+  int nblocks = 0;
+  int block = 0;
+  int team_end = 0;
+  size_t smem = 0;
+  bool empty = false;
+};
+
+// Full launch-time validation in the reference's order (engine.hpp:135-186),
+// then the B200 engine's own limits (HPAC_ERR_UNSUPPORTED).
+int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_t* region,
+            const hpac_spec_t* spec, const hpac_launch_t* launch, Prepared& pr,
+            hpac_stats_t* stats, char* err, size_t el) {
+  int rc;
+  if ((rc = validate_grid(g, err, el))) return rc;
+  if (mapping != HPAC_MAP_PER_THREAD && mapping != HPAC_MAP_PER_TEAM)
+    return fail(err, el, HPAC_ERR_CONFIG, "unknown work mapping");
+  if (n < 0) return fail(err, el, HPAC_ERR_CONFIG, "problem size must be non-negative");
+  const bool per_team = mapping == HPAC_MAP_PER_TEAM;
+  const int64_t cap = per_team ? (int64_t)g->num_teams * g->items_per_thread
+                               : (int64_t)g->num_teams * g->threads_per_team * g->items_per_thread;
+  if (n > cap)
+    return fail(err, el, HPAC_ERR_CONFIG,
+                "grid capacity %lld cannot cover problem size %lld (increase num_teams, "
+                "threads_per_team, or items_per_thread)",
+                (long long)cap, (long long)n);
+  if (!region) return fail(err, el, HPAC_ERR_CONFIG, "region is null");
+  hpac_region_t r = *region;
+  if ((rc = bind_region(&r, err, el))) return rc;
+
+  EngineParams& p = pr.p;
+  std::memset(&p, 0, sizeof p);
+  p.region = r;
+  p.in_dims = r.input_dims;
+  p.out_dims = r.output_dims;
+  p.tech = -1;
+  p.level = HPAC_LEVEL_THREAD;
+  int tpw = 0;
+  if (spec) {
+    if ((rc = validate_spec(spec, err, el))) return rc;
+    p.tech = spec->technique;
+    p.level = spec->level;
+    if (spec->technique == HPAC_TECH_IACT) {
+      if (r.input_dims < 1) return fail(err, el, HPAC_ERR_CONFIG, "iACT requires a region with inputs");
+      tpw = spec->iact_tables_per_warp > 0 ? spec->iact_tables_per_warp : g->warp_size;
+      if (tpw < 1 || g->warp_size % tpw != 0)
+        return fail(err, el, HPAC_ERR_CONFIG, "tables_per_warp (%d) must divide warp_size (%d)",
+                    tpw, g->warp_size);
+    }
+    uint64_t req = 0, avail = 0;
+    rc = arena_account(g, &r, spec, tpw, &req, &avail, err, el);
+    if (stats) {
+      stats->arena_required = req;
+      stats->arena_available = avail;
+    }
+    if (rc) return rc;
+    if (spec->technique == HPAC_TECH_PERFO &&
+        (spec->perfo_kind == HPAC_PERFO_INI || spec->perfo_kind == HPAC_PERFO_FINI) &&
+        r.app == HPAC_APP_TABLE && r.encounters)
+      return fail(err, el, HPAC_ERR_CONFIG,
+                  "INI/FINI perforation requires a fixed trip count per thread");
+    p.taf_h = spec->taf_h_size;
+    p.taf_p = spec->taf_p_size;
+    p.taf_thr = spec->taf_threshold;
+    p.tsize = spec->iact_table_size;
+    p.tpw = tpw;
+    p.iact_thr = spec->iact_threshold;
+    p.perfo_kind = spec->perfo_kind;
+    p.perfo_mod = spec->perfo_modulus;
+    p.perfo_pct = spec->perfo_skip_percent;
+    p.perfo_seed = spec->perfo_seed;
+  }
+  p.voting = spec && p.level != HPAC_LEVEL_THREAD;
+
+  // schedule
+  p.n = n;
+  p.num_teams = g->num_teams;
+  p.tpt = g->threads_per_team;
+  p.ws = g->warp_size;
+  p.wpt = g->threads_per_team / g->warp_size;
+  p.stride = per_team ? (int64_t)g->num_teams : (int64_t)g->num_teams * g->threads_per_team;
+  p.steps = n <= 0 ? 0 : (n + p.stride - 1) / p.stride;
+  p.fast_ws = (p.ws <= 32 && 32 % p.ws == 0) ? 1 : 0;
+  p.has_enc = (r.app == HPAC_APP_TABLE && r.encounters) ? 1 : 0;
+  p.barrier_eval = (r.flags & HPAC_REGION_BARRIER_IN_EVALUATE) ? 1 : 0;
+  p.accumulate = (r.flags & HPAC_REGION_STORE_ACCUMULATE) ? 1 : 0;
+  p.paths = launch ? launch->paths : nullptr;
+
+  int tb = 0, te = g->num_teams;
+  if (launch && (launch->team_begin != 0 || launch->team_end != 0)) {
+    tb = launch->team_begin;
+    te = launch->team_end;
+    if (tb < 0 || te > g->num_teams || tb > te)
+      return fail(err, el, HPAC_ERR_CONFIG, "team range [%d, %d) outside [0, %d)", tb, te,
+                  g->num_teams);
+  }
+  p.team_begin = tb;
+  pr.team_end = te;
+  pr.empty = (te == tb) || n == 0;
+
+  // ---- B200 engine limits ------------------------------------------------
+  if (!per_team) {
+    if (r.app == HPAC_APP_BINOMIAL)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED,
+                  "binomial region runs under per-team mapping (bench/run.hpp:44)");
+    if (g->threads_per_team > 1024)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "threads_per_team > 1024 is not supported");
+    if (r.input_dims > engine_thread_max_in(r.app))
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "region input_dims %d exceeds %d", r.input_dims,
+                  engine_thread_max_in(r.app));
+    if (r.app != HPAC_APP_KMEANS && r.output_dims > engine_thread_max_out(r.app))
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "region output_dims %d exceeds %d",
+                  r.output_dims, engine_thread_max_out(r.app));
+    if (r.app == HPAC_APP_KMEANS && spec && spec->technique == HPAC_TECH_TAF)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "TAF on the K-Means region is not supported");
+    if (r.app == HPAC_APP_KMEANS && spec && spec->technique == HPAC_TECH_IACT && r.out)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED,
+                  "iACT on K-Means keeps labels only; pass out = NULL");
+    if (r.app == HPAC_APP_KMEANS) p.out_dims = 1;  // payload = label
+    pr.kind = 0;
+    pr.block = p.tpt;
+    pr.nblocks = te - tb;
+    pr.smem = engine_thread_smem(p);
+  } else {
+    if (r.app == HPAC_APP_KMEANS)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "K-Means region runs under per-thread mapping");
+    if (r.app == HPAC_APP_BINOMIAL) {
+      pr.kind = 2;
+      pr.block = 64;
+      pr.nblocks = te - tb;
+      pr.smem = binomial_team_smem(p);
+    } else {
+      if (r.input_dims > engine_thread_max_in(r.app) ||
+          r.output_dims > engine_thread_max_out(r.app))
+        return fail(err, el, HPAC_ERR_UNSUPPORTED, "region dims exceed the engine limits");
+      pr.kind = 1;
+      pr.block = 128;
+      pr.nblocks = (te - tb + pr.block - 1) / pr.block;
+      pr.smem = engine_team_seq_smem(p, pr.block);
+    }
+  }
+  if (pr.smem > 227 * 1024)
+    return fail(err, el, HPAC_ERR_UNSUPPORTED,
+                "technique state needs %zu bytes of shared memory per CTA (max 232448)", pr.smem);
+  return 0;
+}
+
+cudaError_t launch_prepared(const Prepared& pr, cudaStream_t st) {
+  if (pr.empty) return cudaSuccess;
+  switch (pr.kind) {
+    case 0: return engine_thread_launch(pr.p, pr.nblocks, pr.smem, st);
+    case 1: return engine_team_seq_launch(pr.p, pr.team_end, pr.block, pr.smem, st);
+    case 2: return binomial_team_launch(pr.p, pr.nblocks, pr.smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+void counters_to_stats(const unsigned long long* c, hpac_stats_t* st) {
+  st->total_invocations = c[kCntTotal];
+  st->approx_invocations = c[kCntApprox];
+  st->divergent_warp_steps = c[kCntDivergent];
+  st->total_warp_steps = c[kCntWarpSteps];
+  st->resident_warps = (int32_t)c[kCntResidentWarps];
+}
+
+// Map device-side faults to the reference's exceptions.
+int finish_status(const unsigned long long* c, hpac_stats_t* st, int app, char* err, size_t el) {
+  if (c[kCntBarrierKey] != ~0ull) {
+    st->barrier_divergence_detected = 1;
+    st->fail_step = (int64_t)(c[kCntBarrierKey] >> 32);
+    st->fail_team = (int32_t)(c[kCntBarrierKey] & 0xffffffffu);
+    st->fail_missing = (int32_t)c[kCntBarrierMissing];
+    return fail(err, el, HPAC_ERR_BARRIER_DIVERGENCE,
+                "barrier divergence in team %d at step %lld: %d thread(s) never arrived",
+                st->fail_team, (long long)st->fail_step, st->fail_missing);
+  }
+  if (c[kCntAppError]) {
+    if (app == HPAC_APP_BINOMIAL)
+      return fail(err, el, HPAC_ERR_CONFIG,
+                  "binomial_price: invalid option parameters or lattice outside the "
+                  "risk-neutral range");
+    return fail(err, el, HPAC_ERR_CONFIG, "black_scholes_call: invalid option parameters");
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+HPAC_API int hpac_abi_version(void) { return HPAC_ABI_VERSION; }
+
+HPAC_API const char* hpac_status_name(int status) {
+  switch (status) {
+    case HPAC_OK: return "OK";
+    case HPAC_ERR_CONFIG: return "ConfigError";
+    case HPAC_ERR_ARENA_OVERFLOW: return "ArenaOverflowError";
+    case HPAC_ERR_BARRIER_DIVERGENCE: return "BarrierDivergenceError";
+    case HPAC_ERR_CUDA: return "CudaError";
+    case HPAC_ERR_DIRECTIVE: return "DirectiveError";
+    case HPAC_ERR_UNSUPPORTED: return "Unsupported";
+  }
+  return "?";
+}
+
+// BenchmarkInfo table + resolve_grid, bench/run.hpp:41-97 ("lavamd" is the
+// framework's extension, one box of particles per team).
+HPAC_API int hpac_resolve_grid(const char* benchmark, int64_t n, const hpac_grid_t* ov,
+                               hpac_grid_t* out, int32_t* mapping_out, char* err, size_t el) {
+  struct Info {
+    const char* id;
+    long long default_n;
+    int tpt, ws, ipt, mapping;
+  };
+  static const Info table[] = {
+      {"blackscholes", 65536, 64, 32, 16, HPAC_MAP_PER_THREAD},
+      {"binomial", 16384, 64, 32, 8, HPAC_MAP_PER_TEAM},
+      {"kmeans", 4096, 64, 32, 4, HPAC_MAP_PER_THREAD},
+      {"synthetic-constant", 16384, 64, 32, 32, HPAC_MAP_PER_THREAD},
+      {"synthetic-slow-drift", 16384, 64, 32, 32, HPAC_MAP_PER_THREAD},
+      {"synthetic-noise", 16384, 64, 32, 32, HPAC_MAP_PER_THREAD},
+  };
+  if (!benchmark) return fail(err, el, HPAC_ERR_CONFIG, "benchmark is null");
+  const Info* info = nullptr;
+  for (const Info& i : table)
+    if (std::strcmp(i.id, benchmark) == 0) info = &i;
+  if (!info) return fail(err, el, HPAC_ERR_CONFIG, "unknown benchmark '%s'", benchmark);
+  hpac_grid_t z{};
+  if (!ov) ov = &z;
+  long long nn = n > 0 ? n : info->default_n;
+  hpac_grid_t g;
+  g.threads_per_team = ov->threads_per_team > 0 ? ov->threads_per_team : info->tpt;
+  g.warp_size = ov->warp_size > 0 ? ov->warp_size : info->ws;
+  g.items_per_thread = ov->items_per_thread > 0 ? ov->items_per_thread : info->ipt;
+  g.shared_mem_budget_bytes = ov->shared_mem_budget_bytes ? ov->shared_mem_budget_bytes : 48 * 1024;
+  if (ov->num_teams > 0) {
+    g.num_teams = ov->num_teams;
+  } else {
+    long long per_team = info->mapping == HPAC_MAP_PER_TEAM
+                             ? g.items_per_thread
+                             : (long long)g.threads_per_team * g.items_per_thread;
+    long long t = (nn + per_team - 1) / per_team;
+    g.num_teams = (int)(t < 1 ? 1 : t);
+  }
+  *out = g;
+  if (mapping_out) *mapping_out = info->mapping;
+  return HPAC_OK;
+}
+
+HPAC_API int hpac_region_bind(hpac_region_t* region, char* err, size_t el) {
+  if (!region) return fail(err, el, HPAC_ERR_CONFIG, "region is null");
+  return bind_region(region, err, el);
+}
+
+HPAC_API int hpac_arena_required(const hpac_grid_t* g, const hpac_region_t* region,
+                                 const hpac_spec_t* spec, uint64_t* required,
+                                 uint64_t* available, char* err, size_t el) {
+  int rc;
+  if ((rc = validate_grid(g, err, el))) return rc;
+  hpac_region_t r = *region;
+  if ((rc = bind_region(&r, err, el))) return rc;
+  if ((rc = validate_spec(spec, err, el))) return rc;
+  int tpw = spec->iact_tables_per_warp > 0 ? spec->iact_tables_per_warp : g->warp_size;
+  return arena_account(g, &r, spec, tpw, required, available, err, el);
+}
+
+HPAC_API int hpac_run_region(const hpac_grid_t* grid, int64_t n, int32_t mapping,
+                             const hpac_region_t* region, const hpac_spec_t* spec,
+                             const hpac_launch_t* launch, hpac_stats_t* stats, char* err,
+                             size_t el) {
+  hpac_stats_t local{};
+  if (!stats) stats = &local;
+  std::memset(stats, 0, sizeof *stats);
+  if (err && el) err[0] = 0;
+  Prepared pr;
+  int rc = prepare(grid, n, mapping, region, spec, launch, pr, stats, err, el);
+  if (rc) return rc;
+  cudaStream_t st = launch ? (cudaStream_t)launch->stream : nullptr;
+  bool sync = !launch || launch->synchronous;
+  cudaError_t e = scratch_ready();
+  if (e != cudaSuccess) return cuda_fail(err, el, e, "scratch");
+  // counters: zero, barrier key = ~0
+  unsigned long long init[kNumCounters];
+  std::memset(init, 0, sizeof init);
+  init[kCntBarrierKey] = ~0ull;
+  std::memcpy(g_scratch.h_cnt, init, sizeof init);
+  if ((e = cudaMemcpyAsync(g_scratch.d_cnt, g_scratch.h_cnt, sizeof init, cudaMemcpyHostToDevice,
+                           st)) != cudaSuccess)
+    return cuda_fail(err, el, e, "counter init");
+  pr.p.counters = g_scratch.d_cnt;
+  if (sync) cudaEventRecord(g_scratch.ev0, st);
+  if ((e = launch_prepared(pr, st)) != cudaSuccess) return cuda_fail(err, el, e, "kernel launch");
+  if (!sync) {
+    // counters stay on device; hpac_stats_fetch reads them after the stream drains
+    g_scratch.pending = true;
+    g_scratch.pending_stream = st;
+    g_scratch.pending_base = *stats;
+    e = cudaMemcpyAsync(g_scratch.h_cnt, g_scratch.d_cnt, sizeof init, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(err, el, e, "counter readback");
+    return HPAC_OK;
+  }
+  cudaEventRecord(g_scratch.ev1, st);
+  e = cudaMemcpyAsync(g_scratch.h_cnt, g_scratch.d_cnt, sizeof init, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(err, el, e, "counter readback");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(err, el, e, "kernel");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, g_scratch.ev0, g_scratch.ev1);
+  counters_to_stats(g_scratch.h_cnt, stats);
+  stats->kernel_ms = ms;
+  return finish_status(g_scratch.h_cnt, stats, pr.p.region.app, err, el);
+}
+
+HPAC_API int hpac_stats_fetch(hpac_stats_t* stats) {
+  if (!g_scratch.pending) return HPAC_ERR_CONFIG;
+  cudaError_t e = cudaStreamSynchronize(g_scratch.pending_stream);
+  if (e != cudaSuccess) return HPAC_ERR_CUDA;
+  *stats = g_scratch.pending_base;
+  counters_to_stats(g_scratch.h_cnt, stats);
+  g_scratch.pending = false;
+  char buf[8];
+  return finish_status(g_scratch.h_cnt, stats, -1, buf, sizeof buf);
+}
+
+// End-to-end entry with host buffers: H2D inputs, run, D2H outputs.
+HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
+                                  const hpac_region_t* host_region, const hpac_spec_t* spec,
+                                  hpac_stats_t* stats, char* err, size_t el) {
+  if (!host_region) return fail(err, el, HPAC_ERR_CONFIG, "region is null");
+  hpac_region_t r = *host_region;
+  int rc = bind_region(&r, err, el);
+  if (rc) return rc;
+  const size_t nn = (size_t)(n > 0 ? n : 0);
+  size_t in_bytes = 0, tab_bytes = 0, enc_bytes = 0, out_bytes = 0, cen_bytes = 0, lab_bytes = 0;
+  switch (r.app) {
+    case HPAC_APP_TABLE:
+      in_bytes = r.in ? nn * r.input_dims * 8 : 0;
+      tab_bytes = nn * r.output_dims * 8;
+      enc_bytes = r.encounters ? nn * 4 : 0;
+      out_bytes = r.out ? nn * r.output_dims * 8 : 0;
+      break;
+    case HPAC_APP_SYNTHETIC: out_bytes = r.out ? nn * 8 : 0; break;
+    case HPAC_APP_BLACKSCHOLES:
+    case HPAC_APP_BINOMIAL:
+      in_bytes = nn * 40;
+      out_bytes = r.out ? nn * 8 : 0;
+      break;
+    case HPAC_APP_KMEANS:
+      in_bytes = nn * r.kmeans_dims * 8;
+      cen_bytes = (size_t)r.kmeans_k * r.kmeans_dims * 8;
+      out_bytes = r.out ? nn * r.kmeans_k * 8 : 0;
+      lab_bytes = r.labels ? nn * 4 : 0;
+      break;
+  }
+  cudaStream_t st = nullptr;
+  cudaError_t e;
+  std::vector<void*> bufs;
+  auto dalloc = [&](size_t bytes, const void* src, bool copy) -> void* {
+    if (!bytes) return nullptr;
+    void* d = nullptr;
+    if (cudaMallocAsync(&d, bytes, st) != cudaSuccess) return nullptr;
+    bufs.push_back(d);
+    if (copy && src) cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
+    return d;
+  };
+  hpac_region_t d = r;
+  d.in = (const double*)dalloc(in_bytes, r.in, true);
+  d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true);
+  d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true);
+  // outputs start from the caller's contents (skipped items keep them)
+  d.out = (double*)dalloc(out_bytes, r.out, true);
+  d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true);
+  d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true);
+  hpac_launch_t L{};
+  L.stream = st;
+  L.synchronous = 1;
+  rc = hpac_run_region(grid, n, mapping, &d, spec, &L, stats, err, el);
+  if (rc == HPAC_OK) {
+    if (out_bytes) cudaMemcpyAsync(r.out, d.out, out_bytes, cudaMemcpyDeviceToHost, st);
+    if (lab_bytes) cudaMemcpyAsync(r.labels, d.labels, lab_bytes, cudaMemcpyDeviceToHost, st);
+  }
+  for (void* b : bufs) cudaFreeAsync(b, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess && rc == HPAC_OK)
+    rc = cuda_fail(err, el, e, "host entry");
+  return rc;
+}
+
+// ---- metrics (metrics.hpp:17-45), device buffers -------------------------
+HPAC_API int hpac_mape(const double* a, const double* b, int64_t n, void* stream, double* result) {
+  if (n <= 0) {
+    *result = 0.0;
+    return HPAC_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* d_sum;
+  unsigned long long* d_inf;
+  if (cudaMallocAsync(&d_sum, 16, st) != cudaSuccess) return HPAC_ERR_CUDA;
+  d_inf = reinterpret_cast<unsigned long long*>(d_sum + 1);
+  cudaMemsetAsync(d_sum, 0, 16, st);
+  if (mape_launch(a, b, n, d_sum, d_inf, st) != cudaSuccess) return HPAC_ERR_CUDA;
+  double h[2];
+  cudaMemcpyAsync(h, d_sum, 16, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_sum, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return HPAC_ERR_CUDA;
+  unsigned long long infc;
+  std::memcpy(&infc, &h[1], 8);
+  *result = infc ? INFINITY : h[0] / (double)n;
+  return HPAC_OK;
+}
+
+HPAC_API int hpac_mcr(const int32_t* a, const int32_t* b, int64_t n, void* stream, double* result) {
+  if (n <= 0) {
+    *result = 0.0;
+    return HPAC_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* d;
+  if (cudaMallocAsync(&d, 8, st) != cudaSuccess) return HPAC_ERR_CUDA;
+  cudaMemsetAsync(d, 0, 8, st);
+  if (mcr_launch(a, b, n, d, st) != cudaSuccess) return HPAC_ERR_CUDA;
+  unsigned long long h;
+  cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return HPAC_ERR_CUDA;
+  *result = (double)h / (double)n;
+  return HPAC_OK;
+}
