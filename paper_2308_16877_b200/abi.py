@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libhpac_b200.so"
+LIB_PATH = Path(os.environ.get("HPAC_LIB", PKG / "libhpac_b200.so"))  # HPAC_LIB: tuning builds only
 
 # ---- status / enums (hpac_offload.h) -------------------------------------
 OK, ERR_CONFIG, ERR_ARENA_OVERFLOW, ERR_BARRIER_DIVERGENCE, ERR_CUDA, ERR_DIRECTIVE, ERR_UNSUPPORTED = range(7)

@@ -237,22 +237,34 @@ __global__ void __launch_bounds__(128) engine_team_seq_kernel(const EngineParams
 // ===========================================================================
 // Binomial options: warp-cooperative register-blocked CRR lattice.
 // ===========================================================================
+#ifndef HPAC_LAT_FPMAX_ODD
+#define HPAC_LAT_FPMAX_ODD 1  // odd nodes compare on the FP64 pipe (balances pipes)
+#endif
+
 struct LatParams {
   double K;
   double pd, qd;  // disc * p, disc * (1 - p)
-  double up, up2, lnu, S;
+  double up, up2, up4, lnu, S;
+  double c1, c2, c4;  // x recurrence offsets: +-K*(1 - up^m), m = 1, 2, 4
 };
 
-template <bool AM, bool PUT>
-__device__ __forceinline__ double lat_node(double vl, double vr, double s, const LatParams& q) {
-  double cont = fma(q.pd, vr, q.qd * vl);
-  if (!AM) return cont;
-  double x = PUT ? q.K - s : s - q.K;
-  // cont >= +0 always, so signed-integer order on the bit patterns equals
-  // max(cont, max(x, 0)) (binomial.hpp:42-44) without an FP64-pipe compare.
+__device__ __forceinline__ void lat_offsets(LatParams& q, bool put) {
+  q.up4 = q.up2 * q.up2;
+  const double sg = put ? 1.0 : -1.0;
+  q.c1 = sg * q.K * (1.0 - q.up);
+  q.c2 = sg * q.K * (1.0 - q.up2);
+  q.c4 = sg * q.K * (1.0 - q.up4);
+}
+
+// max(cont, x) where cont >= +0 always: signed-integer order of the bit
+// patterns equals the double order when one operand is non-negative, so the
+// compare+select runs on the integer pipe instead of the FP64 pipe
+// (binomial.hpp:42-44: max(cont, max(x, 0))).
+__device__ __forceinline__ double max_nonneg(double cont, double x) {
   long long ci = __double_as_longlong(cont), xi = __double_as_longlong(x);
   return __longlong_as_double(ci > xi ? ci : xi);
 }
+__device__ __forceinline__ double max_fp(double cont, double x) { return cont < x ? x : cont; }
 
 // One phase of the lattice at block size B: lane owns nodes
 // [lane*B, lane*B + B) in registers for every level whose live nodes
@@ -260,24 +272,44 @@ __device__ __forceinline__ double lat_node(double vl, double vr, double s, const
 // phase through this warp's shared-memory node array `xch`, which is the
 // rebalance: the next phase reads the same nodes back in smaller blocks,
 // so the triangle keeps all 32 lanes busy down to the root.
-template <int B, int BMAX, bool AM, bool PUT>
-__device__ __forceinline__ void lat_phase(double (&v)[BMAX], int& L, int B0, const LatParams& q,
-                                          int lane, double* xch) {
-  if (B > B0 || L < 0 || L + 2 <= 32 * (B - 1)) return;
+template <int B, int BNEXT, int BMAX, bool AM, bool PUT>
+__device__ __forceinline__ void lat_phase(double (&v)[BMAX], int& L, const LatParams& q, int lane,
+                                          double* xch) {
+  // active for levels whose live nodes (0..L+1) need more than 32*BNEXT slots
+  if (L < 0 || L + 2 <= 32 * BNEXT) return;
 #pragma unroll
   for (int i = 0; i < B; ++i) v[i] = xch[lane * B + i];
-  // s0 = S * up^(2*j0 - L) for this lane's first node j0 = lane*B
-  double s0 = q.S * exp((double)(2 * lane * B - L) * q.lnu);
-  while (L >= 0 && L + 2 > 32 * (B - 1)) {
+  // Exercise value of this lane's first node, x = +-(K - S*up^(2*j0 - L)).
+  // Moving one level down multiplies the node price by up, one node up by
+  // up^2, so x follows the affine recurrences x' = fma(x, m, c_m) with
+  // c_m = +-K*(1-m): one FMA per node instead of a multiply and a subtract.
+  double sp = q.S * exp((double)(2 * lane * B - L) * q.lnu);
+  double x0 = PUT ? q.K - sp : sp - q.K;
+  while (L >= 0 && L + 2 > 32 * BNEXT) {
     double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
-    double s = s0;
+    if (!AM) {
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-      double right = (i + 1 < B) ? v[i + 1] : vr;
-      v[i] = lat_node<AM, PUT>(v[i], right, s, q);
-      if (AM) s *= q.up2;
+      for (int i = 0; i < B; ++i) {
+        double right = (i + 1 < B) ? v[i + 1] : vr;
+        v[i] = fma(q.pd, right, q.qd * v[i]);
+      }
+    } else {
+      // two interleaved x chains (even / odd nodes) halve the dependency depth
+      double xa = x0, xb = fma(x0, q.up2, q.c2);
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        double right = (i + 1 < B) ? v[i + 1] : vr;
+        double cont = fma(q.pd, right, q.qd * v[i]);
+        if ((i & 1) == 0) {
+          v[i] = max_nonneg(cont, xa);
+          xa = fma(xa, q.up4, q.c4);
+        } else {
+          v[i] = (HPAC_LAT_FPMAX_ODD) ? max_fp(cont, xb) : max_nonneg(cont, xb);
+          xb = fma(xb, q.up4, q.c4);
+        }
+      }
+      x0 = fma(x0, q.up, q.c1);
     }
-    s0 *= q.up;
     --L;
   }
   __syncwarp();
@@ -286,14 +318,22 @@ __device__ __forceinline__ void lat_phase(double (&v)[BMAX], int& L, int B0, con
   __syncwarp();
 }
 
-template <int B, int BMAX, bool AM, bool PUT>
-__device__ __forceinline__ void lat_chain(double (&v)[BMAX], int& L, int B0, const LatParams& q,
-                                          int lane, double* xch) {
-  if constexpr (B >= 1) {
-    lat_phase<B, BMAX, AM, PUT>(v, L, B0, q, lane, xch);
-    lat_chain<B - 1, BMAX, AM, PUT>(v, L, B0, q, lane, xch);
-  }
+template <int... Bs>
+struct BList {};
+
+// Walk the block sizes largest to smallest; each phase hands its nodes to
+// the next through xch. A geometric set (ratio ~1.2) keeps ~91% of the
+// lanes busy while the whole chain stays ~20 KB of SASS (the full 33-size
+// chain is ~70 KB and thrashes the instruction cache: ncu "no_instruction").
+template <int BMAX, bool AM, bool PUT, int B, int... REST>
+__device__ __forceinline__ void lat_chain(double (&v)[BMAX], int& L, const LatParams& q, int lane,
+                                          double* xch, BList<B, REST...>) {
+  constexpr int nexts[] = {REST..., 0};
+  lat_phase<B, nexts[0], BMAX, AM, PUT>(v, L, q, lane, xch);
+  if constexpr (sizeof...(REST) > 0) lat_chain<BMAX, AM, PUT>(v, L, q, lane, xch, BList<REST...>{});
 }
+
+using LatBlocks = BList<33, 28, 24, 20, 17, 14, 12, 10, 8, 7, 6, 5, 4, 3, 2, 1>;
 
 // binomial_price (bench/binomial.hpp:16-50) by one warp; every lane
 // returns the price. `xch` = 32*BMAX doubles of this warp's shared memory.
@@ -325,6 +365,7 @@ __device__ double binomial_warp_price(const double* o, int N, double* xch, bool&
   q.up2 = up * up;
   q.lnu = lnu;
   q.S = spot;
+  lat_offsets(q, PUT);
   const int B0 = (N + 1 + 31) / 32;
   // leaves: intrinsic at S * up^(2j - N), j = 0..N (nodes beyond N are dead)
   for (int j = lane; j < 32 * B0; j += 32) {
@@ -335,7 +376,7 @@ __device__ double binomial_warp_price(const double* o, int N, double* xch, bool&
   __syncwarp();
   double v[BMAX];
   int L = N - 1;
-  lat_chain<BMAX, BMAX, AM, PUT>(v, L, B0, q, lane, xch);
+  lat_chain<BMAX, AM, PUT>(v, L, q, lane, xch, LatBlocks{});
   double r = xch[0];
   __syncwarp();
   return r;
@@ -379,7 +420,8 @@ __device__ double binomial_warp_price_smem(const double* o, int N, double* buf, 
   for (int L = N - 1; L >= 0; --L) {
     for (int j = lane; j <= L; j += 32) {
       double s = spot * exp((double)(2 * j - L) * lnu);
-      b[j] = lat_node<AM, PUT>(a[j], a[j + 1], s, q);
+      double cont = fma(q.pd, a[j + 1], q.qd * a[j]);
+      b[j] = AM ? max_nonneg(cont, PUT ? strike - s : s - strike) : cont;
     }
     __syncwarp();
     double* t = a;
@@ -394,6 +436,9 @@ __device__ double binomial_warp_price_smem(const double* o, int N, double* buf, 
 constexpr int kLatBmax = 33;  // register lattice up to N = 32*33 - 1 = 1055 steps
 constexpr int kBinoChunk = 256;
 constexpr int kBinoWarps = 2;  // = threads_per_team / 32 at the default tpt 64
+#ifndef HPAC_BINO_MIN_CTAS
+#define HPAC_BINO_MIN_CTAS 4
+#endif
 
 // Decision codes in the chunk plan.
 constexpr int kActSkip = -1;
@@ -402,7 +447,7 @@ constexpr int kActMiss = -2;
 // <= -3: hit on a step s of this chunk -> -(3 + s)                    [kHitNew]
 
 template <int TECH, bool AM, bool PUT>
-__global__ void __launch_bounds__(kBinoWarps * 32) binomial_team_kernel(const EngineParams p) {
+__global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_team_kernel(const EngineParams p) {
   extern __shared__ __align__(16) double smem[];
   const int team = p.team_begin + (int)blockIdx.x;
   const int warp = threadIdx.x >> 5;

@@ -143,11 +143,14 @@ int validate_spec(const hpac_spec_t* s, char* err, size_t el) {
 }
 
 // Region dims from the app (engine.hpp:26-33 input_dims/output_dims).
-int bind_region(hpac_region_t* r, char* err, size_t el) {
+int bind_region(hpac_region_t* r, char* err, size_t el, int64_t n = 1) {
+  // buffers are only required for non-empty launches (an empty device
+  // array may legitimately be NULL)
+  const bool need = n > 0;
   switch (r->app) {
     case HPAC_APP_TABLE:
-      if (!r->table_out) return fail(err, el, HPAC_ERR_CONFIG, "region has no evaluate function");
-      if (r->input_dims > 0 && !r->in)
+      if (need && !r->table_out) return fail(err, el, HPAC_ERR_CONFIG, "region has no evaluate function");
+      if (need && r->input_dims > 0 && !r->in)
         return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
       if (r->output_dims < 1)
         return fail(err, el, HPAC_ERR_CONFIG, "region output_dims must be >= 1");
@@ -162,19 +165,19 @@ int bind_region(hpac_region_t* r, char* err, size_t el) {
     case HPAC_APP_BLACKSCHOLES:
       r->input_dims = 5;
       r->output_dims = 1;
-      if (!r->in) return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
+      if (need && !r->in) return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
       return 0;
     case HPAC_APP_BINOMIAL:
       r->input_dims = 5;
       r->output_dims = 1;
-      if (!r->in) return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
+      if (need && !r->in) return fail(err, el, HPAC_ERR_CONFIG, "region declares inputs but has no load_input");
       if (r->binomial_steps < 1)
         return fail(err, el, HPAC_ERR_CONFIG, "binomial_price: n_steps must be >= 1");
       return 0;
     case HPAC_APP_KMEANS:
       if (r->kmeans_dims < 1 || r->kmeans_k < 1)
         return fail(err, el, HPAC_ERR_CONFIG, "kmeans dims and k must be >= 1");
-      if (!r->in || !r->centroids)
+      if (need && (!r->in || !r->centroids))
         return fail(err, el, HPAC_ERR_CONFIG, "kmeans region needs points and centroids");
       r->input_dims = r->kmeans_dims;
       r->output_dims = r->kmeans_k;
@@ -258,7 +261,7 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
                 (long long)cap, (long long)n);
   if (!region) return fail(err, el, HPAC_ERR_CONFIG, "region is null");
   hpac_region_t r = *region;
-  if ((rc = bind_region(&r, err, el))) return rc;
+  if ((rc = bind_region(&r, err, el, n))) return rc;
 
   EngineParams& p = pr.p;
   std::memset(&p, 0, sizeof p);
