@@ -1,6 +1,4 @@
-// temporary stubs
+// temporary stub (replaced by kmeans.cu)
 #include "hpac_offload.h"
 #define HPAC_API extern "C" __attribute__((visibility("default")))
-HPAC_API int hpac_parse_directive(const char*, hpac_spec_t*, int32_t*, int64_t*, char*, size_t) { return HPAC_ERR_UNSUPPORTED; }
-HPAC_API int hpac_unparse(const hpac_spec_t*, char*, size_t) { return HPAC_ERR_UNSUPPORTED; }
 HPAC_API int hpac_kmeans_run(const hpac_grid_t*, const hpac_kmeans_problem_t*, const hpac_spec_t*, void*, hpac_kmeans_result_t*, char*, size_t) { return HPAC_ERR_UNSUPPORTED; }
