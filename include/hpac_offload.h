@@ -224,28 +224,37 @@ int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
 int hpac_stats_fetch(hpac_stats_t* stats);
 
 /* ---- K-Means Lloyd loop (bench/kmeans.hpp:62-144) ---------------------- */
+/* Sum-reduction hook for the per-iteration centroid partials: a packed
+   device buffer [k*dims sums | k counts | 1 changed] (doubles). Multi-GPU
+   callers all-reduce it across ranks (e.g. ncclAllReduce / torch
+   all_reduce over NCCL); NULL = single device. */
+typedef void (*hpac_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
+
 typedef struct hpac_kmeans_problem {
-  int64_t n_points;
+  int64_t n_points;     /* points in this shard */
   int32_t dims;
   int32_t k;
-  const double* points; /* device, n*dims */
-  double* centroids;    /* device, k*dims; in: unused (Forgy init), out: final */
+  const double* points; /* device, n*dims (AoS) */
+  double* centroids;    /* device, k*dims; in: initial centroids when
+                           HPAC_KMEANS_CENTROIDS_GIVEN, else Forgy init from
+                           the first k points (kmeans.hpp:66-71); out: final */
   int32_t* assignments; /* device, n labels (out) */
   int32_t max_iters;
-  int32_t flags;        /* HPAC_REGION_KMEANS_FAST_MATH */
+  int32_t flags;        /* HPAC_REGION_KMEANS_FAST_MATH | HPAC_KMEANS_CENTROIDS_GIVEN */
   uint64_t perfo_seed_base; /* RANDOM perforation: seed of iteration i = base + i */
-  /* multi-GPU: when comm != NULL the per-iteration sums/counts are all-reduced
-     with NCCL over this communicator (ncclComm_t); each rank holds its shard */
-  void* nccl_comm;
-  int64_t global_offset; /* index of this shard's first point in the global problem */
-  int64_t global_n;      /* global problem size (decisions keep the global grid) */
+  hpac_allreduce_fn allreduce;
+  void* allreduce_user;
+  double* reduce_buf;   /* optional device buffer of k*dims + k + 1 doubles */
 } hpac_kmeans_problem_t;
 
+#define HPAC_KMEANS_CENTROIDS_GIVEN 8
+
 typedef struct hpac_kmeans_result {
-  int32_t iterations;
-  int32_t converged;
-  hpac_stats_t stats; /* summed over launches */
-  double kernel_ms;
+  int32_t iterations;  /* region launches executed */
+  int32_t converged;   /* stopped because no label changed */
+  hpac_stats_t stats;  /* summed over launches */
+  double region_ms;    /* device time in the distance region kernels */
+  double update_ms;    /* device time in the centroid update kernels */
 } hpac_kmeans_result_t;
 
 int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_t* problem,

@@ -76,16 +76,21 @@ class Launch(C.Structure):
                 ("paths", C.c_void_p), ("synchronous", C.c_int32), ("reserved", C.c_int32)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+KMEANS_CENTROIDS_GIVEN = 8
+
+
 class KmeansProblem(C.Structure):
     _fields_ = [("n_points", C.c_int64), ("dims", C.c_int32), ("k", C.c_int32),
                 ("points", C.c_void_p), ("centroids", C.c_void_p), ("assignments", C.c_void_p),
                 ("max_iters", C.c_int32), ("flags", C.c_int32), ("perfo_seed_base", C.c_uint64),
-                ("nccl_comm", C.c_void_p), ("global_offset", C.c_int64), ("global_n", C.c_int64)]
+                ("allreduce", ALLREDUCE_FN), ("allreduce_user", C.c_void_p),
+                ("reduce_buf", C.c_void_p)]
 
 
 class KmeansResult(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("stats", Stats),
-                ("kernel_ms", C.c_double)]
+                ("region_ms", C.c_double), ("update_ms", C.c_double)]
 
 
 def _declare(lib):

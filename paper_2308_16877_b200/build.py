@@ -60,7 +60,26 @@ def build(verbose: bool = False) -> Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    _build_cpp_tests(verbose)
     return LIB
+
+
+def _build_cpp_tests(verbose: bool = False):
+    """C++ host-API test driver (tests/cpp), linked against the in-tree .so."""
+    src = ROOT / "tests" / "cpp" / "test_engine_cpp.cpp"
+    exe = src.with_suffix("")
+    deps = [src, ROOT / "include" / "hpac" / "hpac.hpp", LIB]
+    if exe.exists() and exe.stat().st_mtime > max(p.stat().st_mtime for p in deps):
+        return exe
+    cmd = [NVCC, "-std=c++17", "-O2", "-x", "c++", "-I", str(ROOT / "include"), str(src),
+           "-Xcompiler", "-ffp-contract=off", "-L", str(PKG), "-lhpac_b200",
+           "-Xlinker", "-rpath=$ORIGIN/../../paper_2308_16877_b200", "-o", str(exe)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
+    return exe
 
 
 if __name__ == "__main__":

@@ -1,0 +1,240 @@
+// kmeans.cu — the K-Means Lloyd loop on the device (kmeans_benchmark,
+// bench/kmeans.hpp:62-144), driving the approximate distance region once per
+// iteration exactly like the reference: technique state is fresh every
+// launch, convergence = no label changed, empty clusters keep their centroid.
+//
+// Labels-only equivalence: the reference stores all k
+// distances per point and argmins them after the launch; a point the region
+// skipped keeps its previous distances, hence its previous argmin. We keep
+// that argmin ("dist label", initialised to 0 = argmin of the zero-filled
+// distance matrix) instead of n*k doubles.
+//
+// Centroid update: one warp per contiguous chunk of points, lane = dimension
+// (coalesced 256 B rows), per-warp private shared-memory accumulators (no
+// atomics), then a fixed-order reduction (deterministic run to run). The
+// packed [sums | counts | changed] buffer is the only cross-GPU exchange; the
+// caller's all-reduce hook (NCCL) runs between the partial sums and the
+// centroid recompute.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "engine.h"
+#include "hpac_offload.h"
+
+#define HPAC_API extern "C" __attribute__((visibility("default")))
+
+namespace hpac {
+
+constexpr int kUpdWarps = 4;
+
+__global__ void kmeans_forgy(const double* pts, int64_t n, int dims, int k, double* cent) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k * dims; i += gridDim.x * blockDim.x) {
+    int c = i / dims, d = i % dims;
+    int64_t src = c < n - 1 ? c : n - 1;
+    cent[i] = pts[src * dims + d];
+  }
+}
+
+__global__ void kmeans_init_labels(int32_t* dist_label, int32_t* assign, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    dist_label[i] = 0;
+    assign[i] = -1;
+  }
+}
+
+// Per-CTA partials: [k*dims sums | k counts | changed] into part[cta][...].
+__global__ void __launch_bounds__(kUpdWarps * 32)
+    kmeans_update_partial(const double* pts, const int32_t* dist_label, int32_t* assign,
+                          int64_t n, int dims, int k, int64_t chunk, double* part) {
+  extern __shared__ __align__(16) double acc[];  // [warps][k*dims + k]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int kd = k * dims, stride = kd + k;
+  double* my = acc + (size_t)w * stride;
+  for (int i = lane; i < stride; i += 32) my[i] = 0.0;
+  __syncwarp();
+  const int64_t gw = (int64_t)blockIdx.x * kUpdWarps + w;
+  const int64_t lo = gw * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  unsigned long long changed = 0;
+  for (int64_t i = lo; i < hi; ++i) {
+    const int c = dist_label[i];
+    const double* x = pts + i * dims;
+    double* row = my + (size_t)c * dims;
+    for (int d = lane; d < dims; d += 32) row[d] += __ldcs(x + d);
+    if (lane == 0) {
+      my[kd + c] += 1.0;
+      if (assign[i] != c) {
+        ++changed;
+        assign[i] = c;
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // fixed-order sum over the CTA's warps
+  double* out = part + (size_t)blockIdx.x * (stride + 1);
+  for (int j = threadIdx.x; j < stride; j += blockDim.x) {
+    double s = 0.0;
+    for (int v = 0; v < kUpdWarps; ++v) s += acc[(size_t)v * stride + j];
+    out[j] = s;
+  }
+  __shared__ unsigned long long ch[kUpdWarps];
+  if (lane == 0) ch[w] = changed;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int v = 0; v < kUpdWarps; ++v) t += ch[v];
+    out[stride] = (double)t;
+  }
+}
+
+// Fixed-order sum over CTAs -> red[j] (deterministic).
+__global__ void kmeans_reduce_partials(const double* part, int nparts, int width, double* red) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < width; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * width + j];
+    red[j] = s;
+  }
+}
+
+// centroids[c] = sums[c] / counts[c]; empty clusters keep theirs (kmeans.hpp:142-143)
+__global__ void kmeans_recompute(const double* red, int dims, int k, double* cent) {
+  const int kd = k * dims;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kd; i += gridDim.x * blockDim.x) {
+    double cnt = red[kd + i / dims];
+    if (cnt > 0.0) cent[i] = red[i] / cnt;
+  }
+}
+
+}  // namespace hpac
+
+namespace {
+int kfail(char* err, size_t len, int code, const char* fmt, ...) {
+  if (err && len) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, len, fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+}  // namespace
+
+HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_t* pb,
+                             const hpac_spec_t* spec, void* stream, hpac_kmeans_result_t* res,
+                             char* err, size_t el) {
+  using namespace hpac;
+  if (!grid || !pb || !res) return kfail(err, el, HPAC_ERR_CONFIG, "null argument");
+  std::memset(res, 0, sizeof *res);
+  const int64_t n = pb->n_points;
+  const int dims = pb->dims, k = pb->k;
+  if (n < 0 || dims < 1 || k < 1 || pb->max_iters < 0)
+    return kfail(err, el, HPAC_ERR_CONFIG, "kmeans problem: bad sizes");
+  const size_t stride = (size_t)k * dims + k;
+  const size_t upd_smem = (size_t)kUpdWarps * stride * sizeof(double);
+  if (upd_smem > 200 * 1024)
+    return kfail(err, el, HPAC_ERR_UNSUPPORTED, "k*dims too large for the centroid update (%zu B)",
+                 upd_smem);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  int32_t* dist_label = nullptr;
+  double* part = nullptr;
+  double* red = pb->reduce_buf;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nparts = sms * 2;
+  const int64_t warps = (int64_t)nparts * kUpdWarps;
+  const int64_t chunk = n > 0 ? (n + warps - 1) / warps : 1;
+  auto cleanup = [&]() {
+    if (dist_label) cudaFreeAsync(dist_label, st);
+    if (part) cudaFreeAsync(part, st);
+    if (red && red != pb->reduce_buf) cudaFreeAsync(red, st);
+  };
+  if ((e = cudaMallocAsync(&dist_label, sizeof(int32_t) * (size_t)(n > 0 ? n : 1), st)) ||
+      (e = cudaMallocAsync(&part, sizeof(double) * (stride + 1) * nparts, st)) ||
+      (!red && (e = cudaMallocAsync(&red, sizeof(double) * (stride + 1), st)))) {
+    cleanup();
+    return kfail(err, el, HPAC_ERR_CUDA, "kmeans alloc: %s", cudaGetErrorString(e));
+  }
+  if (upd_smem > 48 * 1024)
+    cudaFuncSetAttribute(kmeans_update_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)upd_smem);
+  if (!(pb->flags & HPAC_KMEANS_CENTROIDS_GIVEN) && n > 0)
+    kmeans_forgy<<<(k * dims + 255) / 256, 256, 0, st>>>(pb->points, n, dims, k, pb->centroids);
+  kmeans_init_labels<<<sms * 4, 256, 0, st>>>(dist_label, pb->assignments, n);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+
+  hpac_region_t r{};
+  r.app = HPAC_APP_KMEANS;
+  r.kmeans_dims = dims;
+  r.kmeans_k = k;
+  r.flags = pb->flags & HPAC_REGION_KMEANS_FAST_MATH;
+  r.in = pb->points;
+  r.centroids = pb->centroids;
+  r.labels = dist_label;
+  hpac_spec_t sp{};
+  if (spec) sp = *spec;
+  hpac_launch_t L{};
+  L.stream = st;
+  L.synchronous = 1;
+  int rc = HPAC_OK;
+  double h_changed = 0.0;
+  for (int iter = 1; iter <= pb->max_iters; ++iter) {
+    if (spec && spec->technique == HPAC_TECH_PERFO && spec->perfo_kind == HPAC_PERFO_RANDOM)
+      sp.perfo_seed = pb->perfo_seed_base + (uint64_t)iter;
+    hpac_stats_t s{};
+    rc = hpac_run_region(grid, n, HPAC_MAP_PER_THREAD, &r, spec ? &sp : nullptr, &L, &s, err, el);
+    if (rc) {
+      res->stats.arena_required = s.arena_required;
+      res->stats.arena_available = s.arena_available;
+      break;
+    }
+    res->stats.total_invocations += s.total_invocations;
+    res->stats.approx_invocations += s.approx_invocations;
+    res->stats.divergent_warp_steps += s.divergent_warp_steps;
+    res->stats.total_warp_steps += s.total_warp_steps;
+    res->stats.resident_warps = s.resident_warps;
+    res->region_ms += s.kernel_ms;
+    res->iterations = iter;
+    // labels -> assignments, change count, partial sums (every point, as the
+    // reference sums all points in order, kmeans.hpp:135-141)
+    cudaEventRecord(e0, st);
+    kmeans_update_partial<<<nparts, kUpdWarps * 32, upd_smem, st>>>(
+        pb->points, dist_label, pb->assignments, n, dims, k, chunk, part);
+    kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, st>>>(part, nparts,
+                                                                              (int)(stride + 1), red);
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+      rc = kfail(err, el, HPAC_ERR_CUDA, "kmeans update: %s", cudaGetErrorString(e));
+      break;
+    }
+    if (pb->allreduce) pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, st);
+    cudaMemcpyAsync(&h_changed, red + stride, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(e1, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      rc = kfail(err, el, HPAC_ERR_CUDA, "kmeans iteration: %s", cudaGetErrorString(e));
+      break;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    res->update_ms += ms;
+    if (h_changed == 0.0) {  // no observation changed cluster (kmeans.hpp:122-127)
+      res->converged = 1;
+      break;
+    }
+    kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, st>>>(red, dims, k, pb->centroids);
+  }
+  res->stats.kernel_ms = res->region_ms + res->update_ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cleanup();
+  cudaError_t fe = cudaStreamSynchronize(st);
+  if (rc == HPAC_OK && fe != cudaSuccess)
+    rc = kfail(err, el, HPAC_ERR_CUDA, "kmeans: %s", cudaGetErrorString(fe));
+  return rc;
+}

@@ -323,6 +323,55 @@ def arena_required(grid: GridConfig, region: Region, spec):
     return req.value
 
 
+# ---- K-Means Lloyd loop -----------------------------------------------------
+
+@dataclass
+class KmeansResult:
+    assignments: object
+    centroids: object
+    iterations: int
+    converged: bool
+    stats: dict
+    region_ms: float
+    update_ms: float
+
+
+def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=None,
+               fast_math=False, perfo_seed_base=0, allreduce=None, stream=None) -> KmeansResult:
+    """kmeans_benchmark (bench/kmeans.hpp:62-144) on the device. `points` is a
+    torch CUDA tensor n x d. `allreduce(buf_tensor)` (optional) all-reduces the
+    packed [sums | counts | changed] partials across ranks each iteration."""
+    import torch
+    n, d = points.shape
+    cent = torch.empty((k, d), dtype=torch.float64, device=points.device) if centroids is None else centroids
+    assign = torch.empty(n, dtype=torch.int32, device=points.device)
+    red = torch.empty(k * d + k + 1, dtype=torch.float64, device=points.device)
+    pb = abi.KmeansProblem()
+    pb.n_points, pb.dims, pb.k = n, d, k
+    pb.points, pb.centroids, pb.assignments = _ptr(points), _ptr(cent), _ptr(assign)
+    pb.max_iters = max_iters
+    pb.flags = (abi.REGION_KMEANS_FAST_MATH if fast_math else 0) | \
+        (abi.KMEANS_CENTROIDS_GIVEN if centroids is not None else 0)
+    pb.perfo_seed_base = perfo_seed_base
+    pb.reduce_buf = _ptr(red)
+    cb = None
+    if allreduce is not None:
+        def _cb(buf, count, user, st):
+            allreduce(red)
+        cb = abi.ALLREDUCE_FN(_cb)
+        pb.allreduce = cb
+    res = abi.KmeansResult()
+    err = C.create_string_buffer(1024)
+    st = stream if isinstance(stream, int) else (stream.cuda_stream if stream is not None else None)
+    rc = abi.lib().hpac_kmeans_run(C.byref(grid.c()), C.byref(pb),
+                                   C.byref(spec) if spec is not None else None, st,
+                                   C.byref(res), err, 1024)
+    if rc:
+        _raise(rc, err, res.stats)
+    return KmeansResult(assign, cent, res.iterations, bool(res.converged), res.stats.as_dict(),
+                        res.region_ms, res.update_ms)
+
+
 # ---- generators (host) -----------------------------------------------------
 
 def make_bs_portfolio(n, seed, base_block=512, jitter=0.01):
