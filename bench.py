@@ -365,7 +365,11 @@ def our_arm(args, wl):
     ts_exact, st_exact = timed_run(out_exact, None, args.steps, args.warmup)
     clocks = ClockSampler(local)
     clocks.start()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.6:  # untimed load so nvidia-smi sees the clocks
+        E.run_region(grid, n, mapping, mk(out), spec, stream=stream)
     ts_apx, st_apx = timed_run(out, spec, args.steps, args.warmup)
+    time.sleep(0.15)
     clk = clocks.stop()
 
     # quality loss (application metric) vs the exact run
