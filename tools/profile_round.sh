@@ -24,4 +24,13 @@ timeout 600 ncu --set full --import-source on --clock-control none --kernel-name
 timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
   -k 'regex:engine_thread_kernel' -s 2 -c 1 -o $O/${TAG}_km_region -f \
   python bench.py --workload kmeans --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+# reduce reports to CSV pages (the box returns <= 64 MiB); keep only the iACT rep
+for r in $O/${TAG}_*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page raw --csv > ${b}_raw.csv 2>/dev/null
+  ncu -i $r --page details --csv > ${b}_details.csv 2>/dev/null
+  ncu -i $r --page source --csv --print-source sass > ${b}_source.csv 2>/dev/null
+  case $r in *bino_iact*) ;; *) rm -f $r ;; esac
+done
+gzip -f $O/${TAG}_*_source.csv
 ls -la $O
