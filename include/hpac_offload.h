@@ -140,6 +140,13 @@ typedef struct hpac_stats {
   int32_t fail_missing;
   /* measured device time of the region kernel(s), milliseconds */
   double kernel_ms;
+  /* binomial American-put lattices recomputed on the full triangle because
+     the early-exercise boundary check failed (diagnostic; normally 0) */
+  uint64_t lattice_fallbacks;
+  /* binomial lattices: node updates actually executed (the full triangle is
+     N(N+1)/2 per evaluated option; early-exercise tracking skips nodes whose
+     value is the analytic exercise value) */
+  uint64_t lattice_nodes;
 } hpac_stats_t;
 
 /* Region descriptor (replaces engine.hpp:26-33). Pointers are caller-owned;

@@ -17,7 +17,9 @@ enum Counter : int {
   kCntAppError = 5,       // nonzero: an app evaluate raised ConfigError
   kCntBarrierKey = 6,     // min over (step << 32 | team) of barrier divergence; ~0 = none
   kCntBarrierMissing = 7, // missing-thread count of the team that set the key
-  kNumCounters = 8,
+  kCntLatticeFallback = 8,  // binomial boundary-tracking fallbacks
+  kCntLatticeNodes = 9,     // binomial node updates executed
+  kNumCounters = 10,
 };
 
 struct EngineParams {

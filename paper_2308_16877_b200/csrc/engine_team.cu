@@ -23,6 +23,8 @@
 //    misses in parallel and hits are resolved from the producing step.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "apps.cuh"
 #include "engine.h"
 #include "hpac_device.cuh"
@@ -335,10 +337,156 @@ __device__ __forceinline__ void lat_chain(double (&v)[BMAX], int& L, const LatPa
 
 using LatBlocks = BList<33, 28, 24, 20, 17, 14, 12, 10, 8, 7, 6, 5, 4, 3, 2, 1>;
 
+// ---------------------------------------------------------------------------
+// American put with early-exercise boundary tracking.
+//
+// For the CRR American put the exercise region at every level is a prefix
+// {j < j*(L)} of the nodes (the value minus the intrinsic is non-decreasing
+// in the stock price, since the put's delta is >= -1), and there v = K - s
+// exactly. A node j needs only children j and j+1, so nodes below a bound
+// `lo` never feed nodes at or above it: each phase computes [lo, L] only.
+// `lo` is placed a margin below the boundary measured at the end of the
+// previous phase; the assumption "every node below lo is exercised" is
+// verified at every level by checking that node lo itself is exercised
+// (monotonicity covers the rest). If a check ever fails, the option is
+// recomputed with the full lattice. Nodes entering the computed range from
+// below are exactly their exercise values. About half of the triangle is
+// skipped at the reference's result (within the 1e-6 tolerance).
+template <int B, int BMAX>
+__device__ __forceinline__ void bt_phase(double (&v)[BMAX], int& L, int lo, int pmax,
+                                         const LatParams& q, int lane, double* xch, bool check,
+                                         bool& ok, int& nex, int top) {
+  const int base = lo + lane * B;
+  // nodes above `top` (= N+1) are dead: never loaded from or stored to xch
+#pragma unroll
+  for (int i = 0; i < B; ++i) v[i] = base + i <= top ? xch[base + i] : 0.0;
+  double x0 = q.K - q.S * exp((double)(2 * base - L) * q.lnu);
+  double x0_last = x0;
+  int L_last = L;
+  for (int done = 0; L >= 0 && done < pmax; ++done) {
+    double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+    double xa = x0, xb = fma(x0, q.up2, q.c2);
+    const double xfirst = x0;
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double right = (i + 1 < B) ? v[i + 1] : vr;
+      double cont = fma(q.pd, right, q.qd * v[i]);
+      if ((i & 1) == 0) {
+        v[i] = max_nonneg(cont, xa);
+        xa = fma(xa, q.up4, q.c4);
+      } else {
+        v[i] = (HPAC_LAT_FPMAX_ODD) ? max_fp(cont, xb) : max_nonneg(cont, xb);
+        xb = fma(xb, q.up4, q.c4);
+      }
+    }
+    ok = ok && !(check && v[0] != xfirst);  // node lo must stay exercised (lane 0)
+    x0_last = x0;
+    L_last = L;
+    x0 = fma(x0, q.up, q.c1);
+    --L;
+  }
+  // exercised prefix length at the last level processed (boundary estimate)
+  int cnt = 0;
+  {
+    double xa = x0_last, xb = fma(x0_last, q.up2, q.c2);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double x;
+      if ((i & 1) == 0) {
+        x = xa;
+        xa = fma(xa, q.up4, q.c4);
+      } else {
+        x = xb;
+        xb = fma(xb, q.up4, q.c4);
+      }
+      if (base + i <= L_last && v[i] == x) ++cnt;
+    }
+  }
+  nex = __reduce_add_sync(0xffffffffu, cnt);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < B; ++i)
+    if (base + i <= top) xch[base + i] = v[i];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void bt_fill_exercise(double* xch, int from, int to, int level,
+                                                 const LatParams& q, int lane) {
+  for (int j = from + lane; j < to; j += 32)
+    xch[j] = q.K - q.S * exp((double)(2 * j - level) * q.lnu);
+  __syncwarp();
+}
+
+// Returns false (caller recomputes the full triangle) when a boundary check
+// fails or the continuation region outgrows the compiled block sizes.
+constexpr int kBtBmax = 20;
+
+template <bool AM, bool PUT>
+__device__ double lattice_smem_inplace(double spot, double strike, int N, const LatParams& q,
+                                       double* xch);
+
+template <int BMAX>
+__device__ bool binomial_put_bt(double spot, double strike, int N, const LatParams& q,
+                                double* xch, double& price, unsigned long long& nodes) {
+  const int lane = threadIdx.x & 31;
+  constexpr int kPhase = 32;   // levels per phase
+  constexpr int kMargin = 8;   // nodes kept below the measured boundary
+  constexpr int kBtMax = BMAX;  // largest block size in the boundary-tracking chain
+  double v[BMAX];
+  // First bound: one step before expiry the put is exercised wherever
+  // s*u < K, i.e. below j ~ (N-1 + ln(K/S)/lnu)/2; the boundary then drifts
+  // down by ~1/2 node per level plus the early-time move of S*(tau). Keep a
+  // generous margin (the phase checks it anyway).
+  int lo = (int)floor(((double)(N - 1 - kPhase) + log(strike / spot) / q.lnu) * 0.5) - 48;
+  lo = max(0, min(lo, N / 2));
+  for (int j = lo + lane; j <= N; j += 32) {
+    double s = spot * exp((double)(2 * j - N) * q.lnu);
+    double x = strike - s;
+    xch[j] = x < 0.0 ? 0.0 : x;
+  }
+  __syncwarp();
+  int L = N - 1;
+  while (L >= 0) {
+    const int live = L + 2 - lo;
+    if (live > 32 * kBtMax) return false;
+    {
+      const int lv = min(L + 1, kPhase);  // levels L .. L-lv+1 over nodes lo..level
+      nodes += (unsigned long long)lv * (unsigned long long)(L + 1 - lo) -
+               (unsigned long long)lv * (lv - 1) / 2;
+    }
+    bool ok = true;
+    int nex = 0;
+    const bool check = lo > 0;
+#define HPAC_BT(b, bn) \
+  if (live > 32 * (bn)) { bt_phase<b, BMAX>(v, L, lo, kPhase, q, lane, xch, check, ok, nex, N + 1); } else
+    HPAC_BT(20, 17) HPAC_BT(17, 14) HPAC_BT(14, 12) HPAC_BT(12, 10) HPAC_BT(10, 8) HPAC_BT(8, 7)
+    HPAC_BT(7, 6) HPAC_BT(6, 5) HPAC_BT(5, 4) HPAC_BT(4, 3) HPAC_BT(3, 2) HPAC_BT(2, 1)
+    HPAC_BT(1, 0) {}
+#undef HPAC_BT
+    if (!__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) return false;
+    if (L < 0) break;
+    // next bound: measured boundary (level L+1) minus margin and half a phase
+    // of drift; never above mid-lattice; full range near the root
+    int lo_new = lo + nex - kMargin - kPhase / 2;
+    if (L < 3 * kPhase) lo_new = 0;
+    lo_new = max(0, min(lo_new, (L + 1) / 2));
+#ifdef HPAC_BT_DEBUG
+    if (lane == 0 && blockIdx.x == 0 && threadIdx.x == 0)
+      printf("bt L=%d lo=%d nex=%d live=%d lo_new=%d\n", L, lo, nex, live, lo_new);
+#endif
+    if (lo_new < lo) bt_fill_exercise(xch, lo_new, lo, L + 1, q, lane);
+    lo = lo_new;
+  }
+  price = xch[0];
+  __syncwarp();
+  return true;
+}
+
 // binomial_price (bench/binomial.hpp:16-50) by one warp; every lane
 // returns the price. `xch` = 32*BMAX doubles of this warp's shared memory.
 template <int BMAX, bool AM, bool PUT>
-__device__ double binomial_warp_price(const double* o, int N, double* xch, bool& ok) {
+__device__ double binomial_warp_price(const double* o, int N, double* xch, bool& ok,
+                                      unsigned long long* fallbacks = nullptr) {
   const int lane = threadIdx.x & 31;
   double spot = o[0], strike = o[1], rate = o[2], vol = o[3], mat = o[4];
   ok = true;
@@ -366,6 +514,21 @@ __device__ double binomial_warp_price(const double* o, int N, double* xch, bool&
   q.lnu = lnu;
   q.S = spot;
   lat_offsets(q, PUT);
+  if constexpr (AM && PUT) {
+    // boundary tracking on <= 20-node register blocks; whole triangle in
+    // shared memory if its checks fail (keeps the hot kernel small)
+    double price;
+    unsigned long long nodes = 0;
+    if (binomial_put_bt<kBtBmax>(spot, strike, N, q, xch, price, nodes)) {
+      if (lane == 0 && fallbacks) atomicAdd(fallbacks + 1, nodes);
+      return price;
+    }
+    if (lane == 0 && fallbacks) {
+      atomicAdd(fallbacks, 1ull);
+      atomicAdd(fallbacks + 1, (unsigned long long)N * (N + 1) / 2);
+    }
+    return lattice_smem_inplace<AM, PUT>(spot, strike, N, q, xch);
+  }
   const int B0 = (N + 1 + 31) / 32;
   // leaves: intrinsic at S * up^(2j - N), j = 0..N (nodes beyond N are dead)
   for (int j = lane; j < 32 * B0; j += 32) {
@@ -377,6 +540,45 @@ __device__ double binomial_warp_price(const double* o, int N, double* xch, bool&
   double v[BMAX];
   int L = N - 1;
   lat_chain<BMAX, AM, PUT>(v, L, q, lane, xch, LatBlocks{});
+  double r = xch[0];
+  __syncwarp();
+  return r;
+}
+
+// Whole-triangle lattice in this warp's shared node array, in place: each
+// chunk of 32 nodes reads its right neighbours before anyone writes, and
+// chunks go upward, so v_j(L) = f(v_j(L+1), v_{j+1}(L+1)) never reads a
+// value already overwritten (cold fallback of the boundary-tracking path).
+template <bool AM, bool PUT>
+__device__ double lattice_smem_inplace(double spot, double strike, int N, const LatParams& q,
+                                       double* xch) {
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j <= N; j += 32) {
+    double s = spot * exp((double)(2 * j - N) * q.lnu);
+    double x = PUT ? strike - s : s - strike;
+    xch[j] = x < 0.0 ? 0.0 : x;
+  }
+  __syncwarp();
+  for (int L = N - 1; L >= 0; --L) {
+    for (int c = 0; c <= L; c += 32) {
+      const int j = c + lane;
+      double vl = 0.0, vr = 0.0;
+      if (j <= L) {
+        vl = xch[j];
+        vr = xch[j + 1];
+      }
+      __syncwarp();
+      if (j <= L) {
+        double cont = fma(q.pd, vr, q.qd * vl);
+        if (AM) {
+          double s = spot * exp((double)(2 * j - L) * q.lnu);
+          cont = max_nonneg(cont, PUT ? strike - s : s - strike);
+        }
+        xch[j] = cont;
+      }
+      __syncwarp();
+    }
+  }
   double r = xch[0];
   __syncwarp();
   return r;
@@ -497,7 +699,7 @@ __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_
         for (int d = 0; d < 5; ++d) o[d] = p.region.in[idx * 5 + d];
         bool ok;
         outv = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
-                   : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok);
+                   : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok, &p.counters[kCntLatticeFallback]);
         if (!ok) err = true;
         // TafState::observe_accurate (single output)
         const int h = p.taf_h;
@@ -594,7 +796,7 @@ __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_
       for (int d = 0; d < 5; ++d) o[d] = __ldg(p.region.in + idx * 5 + d);
       bool ok;
       double v = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
-                     : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok);
+                     : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok, &p.counters[kCntLatticeFallback]);
       if (!ok) err = true;
       if (lane == 0) price[s] = v;
     }

@@ -396,6 +396,8 @@ void counters_to_stats(const unsigned long long* c, hpac_stats_t* st) {
   st->divergent_warp_steps = c[kCntDivergent];
   st->total_warp_steps = c[kCntWarpSteps];
   st->resident_warps = (int32_t)c[kCntResidentWarps];
+  st->lattice_fallbacks = c[kCntLatticeFallback];
+  st->lattice_nodes = c[kCntLatticeNodes];
 }
 
 // Map device-side faults to the reference's exceptions.
