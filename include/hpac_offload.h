@@ -276,6 +276,11 @@ int hpac_make_binomial_portfolio(int64_t n, uint64_t seed, double jitter,
 int hpac_make_blobs(int64_t n, int32_t dims, int32_t k, uint64_t seed, double separation,
                     double* out /* n*dims */);
 
+/* LavaMD inputs (extension; Rodinia lavaMD init restated): per particle
+   rv = (v, x, y, z) and qv, each value (splitmix64(seed ^ (5*i + c)) % 10 + 1) / 10. */
+int hpac_make_lavamd(int32_t boxes1d, int32_t particles, uint64_t seed, double* rv /* P*4 */,
+                     double* qv /* P */);
+
 /* ---- quality metrics (metrics.hpp:17-45); device buffers --------------- */
 int hpac_mape(const double* accurate, const double* approximate, int64_t n, void* stream,
               double* result);

@@ -386,8 +386,50 @@ typedef struct {
   int64_t n;
 } region_view;
 
+/* LavaMD (extension; the framework's restatement of Rodinia lavaMD, SURVEY
+   Appendix C): the same fixed round-to-nearest exp as the device code. */
+static double lava_exp(double x) {
+  const double kd = rint(x * 1.4426950408889634);
+  const double r = (x + -(kd * 0x1.62e42fee00000p-1)) + -(kd * 0x1.a39ef35793c76p-33);
+  double s = 1.0 / 479001600.0;
+  s = s * r + 1.0 / 39916800.0;
+  s = s * r + 1.0 / 3628800.0;
+  s = s * r + 1.0 / 362880.0;
+  s = s * r + 1.0 / 40320.0;
+  s = s * r + 1.0 / 5040.0;
+  s = s * r + 1.0 / 720.0;
+  s = s * r + 1.0 / 120.0;
+  s = s * r + 1.0 / 24.0;
+  s = s * r + 1.0 / 6.0;
+  s = s * r + 0.5;
+  s = s * r + 1.0;
+  s = s * r + 1.0;
+  return ldexp(s, (int)kd);
+}
+
+/* self first, then the in-grid 26-neighbourhood in (dz, dy, dx) order */
+static int lava_neighbours(int64_t box, int b1, int64_t* nb) {
+  const int bx = (int)(box % b1), by = (int)((box / b1) % b1), bz = (int)(box / ((int64_t)b1 * b1));
+  int c = 0;
+  if (nb) nb[c] = box;
+  ++c;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (!dx && !dy && !dz) continue;
+        int x = bx + dx, y = by + dy, z = bz + dz;
+        if (x < 0 || y < 0 || z < 0 || x >= b1 || y >= b1 || z >= b1) continue;
+        if (nb) nb[c] = ((int64_t)z * b1 + y) * b1 + x;
+        ++c;
+      }
+  return c;
+}
+
+ORACLE_API double oracle_lava_exp(double x) { return lava_exp(x); }
+
 static int region_encounters(const region_view* rv, int64_t idx) {
   if (rv->r->app == HPAC_APP_TABLE && rv->r->encounters) return rv->r->encounters[idx];
+  if (rv->r->app == HPAC_APP_LAVAMD) return lava_neighbours(idx, rv->r->lavamd_boxes1d, NULL);
   return 1;
 }
 
@@ -401,9 +443,36 @@ static void region_load(const region_view* rv, int64_t idx, double* in) {
 }
 
 /* evaluate; returns 0 or an error status (apps throw ConfigError) */
-static int region_eval(const region_view* rv, int64_t idx, double* out, char* err, size_t el) {
+static int region_eval(const region_view* rv, int64_t idx, int lane, int round, double* out,
+                       char* err, size_t el) {
   const hpac_region_t* r = rv->r;
   switch (r->app) {
+    case HPAC_APP_LAVAMD: {
+      const int P = r->lavamd_particles;
+      const double a2 = 2.0 * r->lavamd_alpha * r->lavamd_alpha;
+      int64_t nb[27];
+      lava_neighbours(idx, r->lavamd_boxes1d, nb);
+      const int64_t b = nb[round];
+      const double* me = r->in + (idx * P + lane) * 4;
+      double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+      for (int j = 0; j < P; ++j) {
+        const double* o2 = r->in + (b * P + j) * 4;
+        const double q = r->table_out[b * P + j];
+        const double dot = (me[1] * o2[1] + me[2] * o2[2]) + me[3] * o2[3];
+        const double r2 = (me[0] + o2[0]) - dot;
+        const double vij = lava_exp(-(a2 * r2));
+        const double fs = 2.0 * vij;
+        fv = fv + q * vij;
+        fx = fx + q * (fs * (me[1] - o2[1]));
+        fy = fy + q * (fs * (me[2] - o2[2]));
+        fz = fz + q * (fs * (me[3] - o2[3]));
+      }
+      out[0] = fv;
+      out[1] = fx;
+      out[2] = fy;
+      out[3] = fz;
+      return 0;
+    }
     case HPAC_APP_TABLE:
       for (int d = 0; d < rv->out_dims; ++d) out[d] = r->table_out[(size_t)idx * rv->out_dims + d];
       return 0;
@@ -437,8 +506,13 @@ static int region_eval(const region_view* rv, int64_t idx, double* out, char* er
   return fail(err, el, HPAC_ERR_UNSUPPORTED, "oracle: unsupported app %d", r->app);
 }
 
-static void region_store(const region_view* rv, int64_t idx, const double* out) {
+static void region_store(const region_view* rv, int64_t idx, int lane, const double* out) {
   const hpac_region_t* r = rv->r;
+  if (r->app == HPAC_APP_LAVAMD) {
+    double* f = r->out + (idx * r->lavamd_particles + lane) * 4;
+    for (int c = 0; c < 4; ++c) f[c] = f[c] + out[c];
+    return;
+  }
   if (r->app == HPAC_APP_KMEANS) {
     int k = r->kmeans_k;
     if (r->out)
@@ -478,6 +552,10 @@ static int region_bind(const hpac_region_t* r, region_view* rv, char* err, size_
     case HPAC_APP_KMEANS:
       rv->in_dims = r->kmeans_dims;
       rv->out_dims = r->kmeans_k;
+      return 0;
+    case HPAC_APP_LAVAMD:
+      rv->in_dims = 0;
+      rv->out_dims = 4;
       return 0;
   }
   return fail(err, el, HPAC_ERR_UNSUPPORTED, "oracle: unsupported app %d", r->app);
@@ -626,7 +704,7 @@ ORACLE_API int oracle_run_region(const hpac_grid_t* g, int64_t n, int32_t mappin
   const int64_t stride = per_team ? nteams : total_threads;
   const int64_t steps = n <= 0 ? 0 : (n + stride - 1) / stride;
   const int in_dims = rv.in_dims, out_dims = rv.out_dims;
-  const int has_enc = reg->app == HPAC_APP_TABLE && reg->encounters != NULL;
+  const int has_enc = (reg->app == HPAC_APP_TABLE && reg->encounters != NULL) || reg->app == HPAC_APP_LAVAMD;
   const int barrier_eval = (reg->flags & HPAC_REGION_BARRIER_IN_EVALUATE) != 0;
 
   /* bind_technique, engine.hpp:75-117 */
@@ -799,14 +877,14 @@ ORACLE_API int oracle_run_region(const hpac_grid_t* g, int64_t n, int32_t mappin
             if (approx) {
               if (tech == HPAC_TECH_TAF) {
                 taf_emit(&taf[tid], out);
-                region_store(&rv, lw->idx, out);
+                region_store(&rv, lw->idx, local, out);
               } else if (tech == HPAC_TECH_IACT) {
                 memo_table* t = &tables[warp_id * tpw + lane / (ws / tpw)];
                 if (lw->hit >= 0) {
-                  region_store(&rv, lw->idx, t->out + (size_t)lw->hit * out_dims);
+                  region_store(&rv, lw->idx, local, t->out + (size_t)lw->hit * out_dims);
                 } else if (t->occ > 0) {
                   int s = memo_nearest(t, in);
-                  region_store(&rv, lw->idx, t->out + (size_t)s * out_dims);
+                  region_store(&rv, lw->idx, local, t->out + (size_t)s * out_dims);
                 } else {
                   approx = 0; /* empty table: accurate fallback */
                 }
@@ -814,10 +892,10 @@ ORACLE_API int oracle_run_region(const hpac_grid_t* g, int64_t n, int32_t mappin
               /* perforation skip: output untouched */
             }
             if (!approx) {
-              rc = region_eval(&rv, lw->idx, out, err, el);
+              rc = region_eval(&rv, lw->idx, local, round, out, err, el);
               if (rc) break;
               if (barrier_eval) arrivals[local] += 1;
-              region_store(&rv, lw->idx, out);
+              region_store(&rv, lw->idx, local, out);
               if (tech == HPAC_TECH_TAF) taf_observe(&taf[tid], out);
               if (tech == HPAC_TECH_IACT && lw->hit < 0) miss[nmiss++] = lane;
             }

@@ -7,6 +7,6 @@ from . import abi  # noqa: F401
 from .engine import (  # noqa: F401
     ArenaOverflowError, BarrierDivergenceError, ConfigError, CudaError, DirectiveError,
     GridConfig, KmeansResult, LaunchResult, Region, SimtError, UnsupportedError, WorkMapping, arena_required,
-    binomial_region, blackscholes_region, iact, kmeans_region, kmeans_run, make_binomial_portfolio,
+    binomial_region, blackscholes_region, iact, kmeans_region, kmeans_run, lavamd_region, make_lavamd, make_binomial_portfolio,
     make_blobs, make_bs_portfolio, mape, mcr, parse_directive, perfo, resolve_grid, run_region,
     run_region_host, synthetic_region, table_region, taf, unparse)

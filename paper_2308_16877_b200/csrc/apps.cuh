@@ -31,9 +31,19 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
   return true;
 }
 
+// Hooks every app inherits: encounters per item (Region::encounters,
+// engine.hpp:29; 1 by default) and a per-round staging step executed by
+// every thread of the team outside the approximated region.
+struct AppBase {
+  __device__ static int encounters(const EngineParams& p, int64_t idx) {
+    return p.region.encounters ? p.region.encounters[idx] : 1;
+  }
+  __device__ static void round_begin(const EngineParams&, int64_t, int, double*, bool) {}
+};
+
 // Generic pure region over a work index (HPAC_APP_TABLE): load_input reads
 // `in`, evaluate returns the precomputed accurate output `table_out`.
-struct AppTable {
+struct AppTable : AppBase {
   static constexpr int IN_MAX = 8;
   static constexpr int OUT_MAX = 4;
   __device__ static void load(const EngineParams& p, int64_t idx, double (&in)[IN_MAX]) {
@@ -44,14 +54,14 @@ struct AppTable {
   }
   __device__ static void init(const EngineParams&, double*) {}
   __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&)[IN_MAX],
-                              double (&out)[OUT_MAX], const double*) {
+                              double (&out)[OUT_MAX], const double*, int, int) {
     const double* src = p.region.table_out + idx * p.out_dims;
 #pragma unroll
     for (int d = 0; d < OUT_MAX; ++d)
       if (d < p.out_dims) out[d] = src[d];
     return true;
   }
-  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX]) {
+  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX], int) {
     double* dst = p.region.out;
     if (!dst) return;
     dst += idx * p.out_dims;
@@ -67,7 +77,7 @@ struct AppTable {
 };
 
 // bench/synthetic.hpp:56-71
-struct AppSynthetic {
+struct AppSynthetic : AppBase {
   static constexpr int IN_MAX = 1;
   static constexpr int OUT_MAX = 1;
   __device__ static void load(const EngineParams& p, int64_t idx, double (&in)[IN_MAX]) {
@@ -75,17 +85,17 @@ struct AppSynthetic {
   }
   __device__ static void init(const EngineParams&, double*) {}
   __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&)[IN_MAX],
-                              double (&out)[OUT_MAX], const double*) {
+                              double (&out)[OUT_MAX], const double*, int, int) {
     out[0] = synthetic_eval(synthetic_value(p.region.synthetic_profile, idx, p.region.seed));
     return true;
   }
-  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX]) {
+  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX], int) {
     if (p.region.out) p.region.out[idx] = out[0];
   }
 };
 
 // bench/blackscholes.hpp:72-92 (AoS option = 5 doubles)
-struct AppBlackScholes {
+struct AppBlackScholes : AppBase {
   static constexpr int IN_MAX = 5;
   static constexpr int OUT_MAX = 1;
   __device__ static void load(const EngineParams& p, int64_t idx, double (&in)[IN_MAX]) {
@@ -95,10 +105,10 @@ struct AppBlackScholes {
   }
   __device__ static void init(const EngineParams&, double*) {}
   __device__ static bool eval(const EngineParams&, int64_t, const double (&in)[IN_MAX],
-                              double (&out)[OUT_MAX], const double*) {
+                              double (&out)[OUT_MAX], const double*, int, int) {
     return bs_call(in[0], in[1], in[2], in[3], in[4], out[0]);
   }
-  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX]) {
+  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX], int) {
     if (p.region.out) __stcs(p.region.out + idx, out[0]);
   }
 };
@@ -112,7 +122,7 @@ struct AppBlackScholes {
 // distances and labels are bit-identical to the CPU; the argmin takes a
 // sqrt only when a squared distance improves (sqrt is monotone, so the
 // strict-< / lowest-index result is unchanged).
-struct AppKmeans {
+struct AppKmeans : AppBase {
   static constexpr int IN_MAX = 32;
   static constexpr int OUT_MAX = 1;
   __device__ static void init(const EngineParams& p, double* scratch) {
@@ -138,7 +148,7 @@ struct AppKmeans {
     }
   }
   __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&in)[IN_MAX],
-                              double (&out)[OUT_MAX], const double* cent) {
+                              double (&out)[OUT_MAX], const double* cent, int, int) {
     const int dims = p.region.kmeans_dims, k = p.region.kmeans_k;
     const bool fast = (p.region.flags & HPAC_REGION_KMEANS_FAST_MATH) != 0;
     double* dist = p.region.out ? p.region.out + idx * k : nullptr;
@@ -185,8 +195,122 @@ struct AppKmeans {
     out[0] = (double)best;
     return true;
   }
-  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX]) {
+  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX], int) {
     if (p.region.labels) p.region.labels[idx] = (int32_t)out[0];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// LavaMD (Rodinia lavaMD, restated per SURVEY.md Appendix C; not in the
+// reference, parity against oracle/hpac_oracle.c). Boxes on a boxes1d^3 grid,
+// `particles` per box (= threads_per_team: lane = home particle). Item =
+// home box (per-team mapping); encounter r = neighbour box r (self first,
+// then the 26-neighbourhood in z,y,x order inside the grid). The
+// approximated region is one neighbour box's force contribution to the
+// lane's particle: out = (v, x, y, z) accumulated into fv. Neighbour
+// particles are staged in shared memory by the whole team OUTSIDE the
+// region (round_begin), so thread/warp decisions never skip a barrier.
+// exp() is a fixed round-to-nearest sequence shared with the oracle, so the
+// contributions (and TAF decisions on them) are bit-identical to the CPU.
+__host__ __device__ __forceinline__ double lava_exp(double x) {
+#ifdef __CUDA_ARCH__
+#define LMUL __dmul_rn
+#define LADD __dadd_rn
+#else
+#define LMUL(a, b) ((a) * (b))
+#define LADD(a, b) ((a) + (b))
+#endif
+  const double kd = rint(LMUL(x, 1.4426950408889634));
+  const double r = LADD(LADD(x, -LMUL(kd, 0x1.62e42fee00000p-1)), -LMUL(kd, 0x1.a39ef35793c76p-33));
+  double s = 1.0 / 479001600.0;  // 1/12!
+  s = LADD(LMUL(s, r), 1.0 / 39916800.0);
+  s = LADD(LMUL(s, r), 1.0 / 3628800.0);
+  s = LADD(LMUL(s, r), 1.0 / 362880.0);
+  s = LADD(LMUL(s, r), 1.0 / 40320.0);
+  s = LADD(LMUL(s, r), 1.0 / 5040.0);
+  s = LADD(LMUL(s, r), 1.0 / 720.0);
+  s = LADD(LMUL(s, r), 1.0 / 120.0);
+  s = LADD(LMUL(s, r), 1.0 / 24.0);
+  s = LADD(LMUL(s, r), 1.0 / 6.0);
+  s = LADD(LMUL(s, r), 0.5);
+  s = LADD(LMUL(s, r), 1.0);
+  s = LADD(LMUL(s, r), 1.0);
+  return ldexp(s, (int)kd);
+#undef LMUL
+#undef LADD
+}
+
+__host__ __device__ __forceinline__ int lava_neighbours(int64_t box, int b1, int64_t* nb) {
+  const int bx = (int)(box % b1), by = (int)((box / b1) % b1), bz = (int)(box / ((int64_t)b1 * b1));
+  int c = 0;
+  if (nb) nb[c] = box;
+  ++c;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (!dx && !dy && !dz) continue;
+        const int x = bx + dx, y = by + dy, z = bz + dz;
+        if (x < 0 || y < 0 || z < 0 || x >= b1 || y >= b1 || z >= b1) continue;
+        if (nb) nb[c] = ((int64_t)z * b1 + y) * b1 + x;
+        ++c;
+      }
+  return c;
+}
+
+struct AppLavaMD : AppBase {
+  static constexpr int IN_MAX = 1;
+  static constexpr int OUT_MAX = 4;
+  __device__ static void init(const EngineParams&, double*) {}
+  __device__ static int encounters(const EngineParams& p, int64_t idx) {
+    return lava_neighbours(idx, p.region.lavamd_boxes1d, nullptr);
+  }
+  // stage neighbour box `round` of home box idx: rv (4) + qv (1) per particle
+  __device__ static void round_begin(const EngineParams& p, int64_t idx, int round, double* s,
+                                     bool valid) {
+    __syncthreads();  // previous round's evaluations are done with s
+    if (valid) {
+      int64_t nb[27];
+      const int c = lava_neighbours(idx, p.region.lavamd_boxes1d, nb);
+      if (round < c) {
+        const int P = p.region.lavamd_particles;
+        const int64_t b = nb[round];
+        for (int i = threadIdx.x; i < P * 4; i += blockDim.x) s[i] = __ldg(p.region.in + b * P * 4 + i);
+        for (int i = threadIdx.x; i < P; i += blockDim.x) s[P * 4 + i] = __ldg(p.region.table_out + b * P + i);
+      }
+    }
+    __syncthreads();
+  }
+  __device__ static void load(const EngineParams&, int64_t, double (&)[IN_MAX]) {}
+  __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&)[IN_MAX],
+                              double (&out)[OUT_MAX], const double* s, int local, int) {
+    const int P = p.region.lavamd_particles;
+    const double a2 = __dmul_rn(__dmul_rn(2.0, p.region.lavamd_alpha), p.region.lavamd_alpha);
+    const double* me = p.region.in + (idx * P + local) * 4;
+    const double av = me[0], ax = me[1], ay = me[2], az = me[3];
+    double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+    for (int j = 0; j < P; ++j) {
+      const double bv = s[j * 4], bx = s[j * 4 + 1], by = s[j * 4 + 2], bz = s[j * 4 + 3];
+      const double q = s[P * 4 + j];
+      const double dot = __dadd_rn(__dadd_rn(__dmul_rn(ax, bx), __dmul_rn(ay, by)), __dmul_rn(az, bz));
+      const double r2 = __dsub_rn(__dadd_rn(av, bv), dot);
+      const double vij = lava_exp(-__dmul_rn(a2, r2));
+      const double fs = __dmul_rn(2.0, vij);
+      fv = __dadd_rn(fv, __dmul_rn(q, vij));
+      fx = __dadd_rn(fx, __dmul_rn(q, __dmul_rn(fs, __dsub_rn(ax, bx))));
+      fy = __dadd_rn(fy, __dmul_rn(q, __dmul_rn(fs, __dsub_rn(ay, by))));
+      fz = __dadd_rn(fz, __dmul_rn(q, __dmul_rn(fs, __dsub_rn(az, bz))));
+    }
+    out[0] = fv;
+    out[1] = fx;
+    out[2] = fy;
+    out[3] = fz;
+    return true;
+  }
+  __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX],
+                               int local) {
+    double* f = p.region.out + (idx * p.region.lavamd_particles + local) * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) f[c] = __dadd_rn(f[c], out[c]);
   }
 };
 

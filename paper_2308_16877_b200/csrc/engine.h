@@ -47,6 +47,8 @@ struct EngineParams {
   hpac_region_t region;
   int32_t in_dims, out_dims;
   int32_t has_enc, barrier_eval, accumulate;
+  int32_t per_team;  // lane-level engine under per-team mapping (all lanes share idx)
+  int32_t staged;    // app stages shared data per round (AppLavaMD)
   // shared-memory carve-up (doubles unless noted)
   int32_t smem_taf_off;   // TAF ring (smem variant)
   int32_t smem_last_off;  // TAF last (smem variant)

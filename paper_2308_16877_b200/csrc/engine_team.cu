@@ -86,6 +86,14 @@ __device__ __forceinline__ void team_lookup(const double* tab, int stride, int D
 
 }  // namespace
 
+// Every lane of the team stores (engine.hpp:317,338); only an accumulating
+// store is observable more than once, so repeat it threads_per_team times.
+template <class App, class Out>
+__device__ __forceinline__ void store_team(const EngineParams& p, int64_t idx, const Out& out) {
+  const int reps = p.accumulate ? p.tpt : 1;
+  for (int r = 0; r < reps; ++r) App::store(p, idx, out, r);
+}
+
 // ===========================================================================
 // Scalar apps under per-team mapping: one CUDA thread = one logical team.
 // ===========================================================================
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(128) engine_team_seq_kernel(const EngineParams
 
   for (int64_t step = 0; live && step < trip; ++step) {
     const int64_t idx = team + step * p.stride;
-    const int enc = p.has_enc ? p.region.encounters[idx] : 1;
+    const int enc = p.has_enc ? App::encounters(p, idx) : 1;
     uint8_t pbits = 0;
     for (int round = 0; round < enc; ++round) {
       double in[IN_MAX];
@@ -152,17 +160,17 @@ __global__ void __launch_bounds__(128) engine_team_seq_kernel(const EngineParams
             head = 0;
             mode = kTafFilling;
           }
-          App::store(p, idx, out);
+          store_team<App>(p, idx, out);
         } else if (TECH == HPAC_TECH_IACT) {
 #pragma unroll
           for (int d = 0; d < OUT_MAX; ++d)
             if (d < p.out_dims) out[d] = tab[(hit * D + p.in_dims + d) * stride_s];
-          App::store(p, idx, out);
+          store_team<App>(p, idx, out);
         }
       } else {
         if (!loaded) App::load(p, idx, in);
-        if (!App::eval(p, idx, in, out, nullptr)) err = true;
-        App::store(p, idx, out);
+        if (!App::eval(p, idx, in, out, nullptr, 0, round)) err = true;
+        store_team<App>(p, idx, out);
         if (TECH == HPAC_TECH_TAF) {
           bool full;
           if (HREG > 0) {

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
   const int local = threadIdx.x;
   const int team = p.team_begin + (int)blockIdx.x;
   const int64_t tid = (int64_t)team * p.tpt + local;
+  const int64_t owner = p.per_team ? (int64_t)team : tid;  // machine.hpp:77-80
   const int ws = p.ws;
   const int lane = local % ws;   // logical lane
   const int wloc = local / ws;   // logical warp within the team
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
   int64_t trip = 0;
   if (TECH == HPAC_TECH_PERFO &&
       (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
-    trip = trip_count(tid, p.stride, p.n, p.steps);
+    trip = trip_count(owner, p.stride, p.n, p.steps);
 
   // ---- stats ---------------------------------------------------------------
   unsigned long long s_total = 0, s_approx = 0, s_warp = 0, s_div = 0;
@@ -101,10 +102,10 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
   int round_ctr = 0;  // global round counter for triple buffers
 
   for (int64_t step = 0; step < p.steps; ++step) {
-    const int64_t idx = tid + step * p.stride;
+    const int64_t idx = owner + step * p.stride;
     const bool active = idx < p.n;
     int enc = 1;
-    if (p.has_enc && active) enc = p.region.encounters[idx];
+    if (p.has_enc && active) enc = App::encounters(p, idx);
     int rounds = 1;
     if (p.has_enc) {
       // team max of encounters (engine.hpp:194-215); block-uniform
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
     for (int round = 0; round < rounds; ++round, ++round_ctr) {
       const int buf = round_ctr % 3;
       const bool in_round = active && round < enc;
+      if (p.staged) App::round_begin(p, idx, round, smem + p.smem_scratch_off, active);
 
       // ---- predicate phase (engine.hpp:221-251) ----------------------------
       double in[IN_MAX];
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
           const bool herded = p.perfo_kind == HPAC_PERFO_HERDED_SMALL ||
                               p.perfo_kind == HPAC_PERFO_HERDED_LARGE;
           pred = perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed,
-                                   herded ? hcount : pcount, trip, tid);
+                                   herded ? hcount : pcount, trip, owner);
         }
       }
 
@@ -223,14 +225,14 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
               taf_head = 0;
               taf_mode = kTafFilling;
             }
-            App::store(p, idx, out);
+            App::store(p, idx, out, local);
           } else if (TECH == HPAC_TECH_IACT) {
             int slot = hit >= 0 ? hit : (occ > 0 ? near : -1);
             if (slot >= 0) {
 #pragma unroll
               for (int d = 0; d < OUT_MAX; ++d)
                 if (d < p.out_dims) out[d] = tabs[(slot * D + p.in_dims + d) * T + tab];
-              App::store(p, idx, out);
+              App::store(p, idx, out, local);
             } else {
               approx = false;  // empty table: accurate fallback (engine.hpp:327-331)
             }
@@ -239,9 +241,9 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
         }
         if (!approx) {
           if (!loaded) App::load(p, idx, in);
-          if (!App::eval(p, idx, in, out, smem + p.smem_scratch_off)) app_error = true;
+          if (!App::eval(p, idx, in, out, smem + p.smem_scratch_off, local, round)) app_error = true;
           if (p.barrier_eval) arrivals += 1;
-          App::store(p, idx, out);
+          App::store(p, idx, out, local);
           if (TECH == HPAC_TECH_TAF) {
             // TafState::observe_accurate, taf.hpp:94-108
             bool full;
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
       (void)team_any;
     }
 
-    if (p.paths && active) p.paths[idx] = pbits;
+    if (p.paths && active && (!p.per_team || local == 0)) p.paths[idx] = pbits;
 
     // ---- TeamState::end_step barrier check (machine.hpp:53-61) -------------
     if (p.barrier_eval) {
@@ -490,6 +492,7 @@ size_t engine_thread_smem(EngineParams& p) {
   p.smem_scratch_off = (int)off;
   if (p.region.app == HPAC_APP_KMEANS)
     off += (size_t)p.region.kmeans_k * p.region.kmeans_dims;
+  if (p.region.app == HPAC_APP_LAVAMD) off += (size_t)p.region.lavamd_particles * 5;
   p.smem_ctl_off = (int)off;
   // control ints: 16 fixed + generic-ws words (4 per logical warp + 3 per table)
   size_t ctl_ints = 16 + 4 * (size_t)p.wpt + 3 * (size_t)p.wpt * (p.tpw > 0 ? p.tpw : 1) + 4;
@@ -504,6 +507,7 @@ int engine_thread_max_in(int app) {
     case HPAC_APP_SYNTHETIC: return AppSynthetic::IN_MAX;
     case HPAC_APP_BLACKSCHOLES: return AppBlackScholes::IN_MAX;
     case HPAC_APP_KMEANS: return AppKmeans::IN_MAX;
+    case HPAC_APP_LAVAMD: return 0;
   }
   return 0;
 }
@@ -513,6 +517,7 @@ int engine_thread_max_out(int app) {
     case HPAC_APP_SYNTHETIC: return AppSynthetic::OUT_MAX;
     case HPAC_APP_BLACKSCHOLES: return AppBlackScholes::OUT_MAX;
     case HPAC_APP_KMEANS: return AppKmeans::OUT_MAX;
+    case HPAC_APP_LAVAMD: return AppLavaMD::OUT_MAX;
   }
   return 0;
 }
@@ -524,6 +529,7 @@ cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem
     case HPAC_APP_SYNTHETIC: return launch_app<AppSynthetic>(p, nblocks, smem, st);
     case HPAC_APP_BLACKSCHOLES: return launch_app<AppBlackScholes>(p, nblocks, smem, st);
     case HPAC_APP_KMEANS: return launch_app<AppKmeans>(p, nblocks, smem, st);
+    case HPAC_APP_LAVAMD: return launch_app<AppLavaMD>(p, nblocks, smem, st);
   }
   return cudaErrorInvalidValue;
 }

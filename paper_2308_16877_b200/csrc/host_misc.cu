@@ -11,6 +11,7 @@
 #include <random>
 #include <vector>
 
+#include "hpac_device.cuh"
 #include "hpac_offload.h"
 
 #define HPAC_API extern "C" __attribute__((visibility("default")))
@@ -176,6 +177,24 @@ HPAC_API int hpac_make_binomial_portfolio(int64_t n, uint64_t seed, double jitte
     o[2] = 0.05;
     o[3] = 0.25 * std::abs(wiggle(rng));
     o[4] = 1.0;
+  }
+  return HPAC_OK;
+}
+
+// LavaMD particles (Rodinia lavaMD: (rand() % 10 + 1) / 10 per value).
+HPAC_API int hpac_make_lavamd(int32_t boxes1d, int32_t particles, uint64_t seed, double* rv,
+                              double* qv) {
+  if (boxes1d < 1 || particles < 1 || !rv || !qv) return HPAC_ERR_CONFIG;
+  const int64_t n = (int64_t)boxes1d * boxes1d * boxes1d * particles;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int c = 0; c < 5; ++c) {
+      uint64_t h = hpac::splitmix64(seed ^ (uint64_t)(5 * i + c));
+      double v = (double)(h % 10 + 1) / 10.0;
+      if (c < 4)
+        rv[i * 4 + c] = v;
+      else
+        qv[i] = v;
+    }
   }
   return HPAC_OK;
 }

@@ -182,6 +182,15 @@ int bind_region(hpac_region_t* r, char* err, size_t el, int64_t n = 1) {
       r->input_dims = r->kmeans_dims;
       r->output_dims = r->kmeans_k;
       return 0;
+    case HPAC_APP_LAVAMD:
+      if (r->lavamd_boxes1d < 1 || r->lavamd_particles < 1)
+        return fail(err, el, HPAC_ERR_CONFIG, "lavamd: boxes1d and particles must be >= 1");
+      if (!(r->lavamd_alpha > 0.0)) return fail(err, el, HPAC_ERR_CONFIG, "lavamd: alpha must be > 0");
+      if (need && (!r->in || !r->table_out || !r->out))
+        return fail(err, el, HPAC_ERR_CONFIG, "lavamd region needs rv (in), qv (table_out) and fv (out)");
+      r->input_dims = 0;
+      r->output_dims = 4;
+      return 0;
   }
   return fail(err, el, HPAC_ERR_UNSUPPORTED, "unsupported application id %d", r->app);
 }
@@ -291,7 +300,7 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
     if (rc) return rc;
     if (spec->technique == HPAC_TECH_PERFO &&
         (spec->perfo_kind == HPAC_PERFO_INI || spec->perfo_kind == HPAC_PERFO_FINI) &&
-        r.app == HPAC_APP_TABLE && r.encounters)
+        ((r.app == HPAC_APP_TABLE && r.encounters) || r.app == HPAC_APP_LAVAMD))
       return fail(err, el, HPAC_ERR_CONFIG,
                   "INI/FINI perforation requires a fixed trip count per thread");
     p.taf_h = spec->taf_h_size;
@@ -316,7 +325,8 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
   p.stride = per_team ? (int64_t)g->num_teams : (int64_t)g->num_teams * g->threads_per_team;
   p.steps = n <= 0 ? 0 : (n + p.stride - 1) / p.stride;
   p.fast_ws = (p.ws <= 32 && 32 % p.ws == 0) ? 1 : 0;
-  p.has_enc = (r.app == HPAC_APP_TABLE && r.encounters) ? 1 : 0;
+  p.has_enc = ((r.app == HPAC_APP_TABLE && r.encounters) || r.app == HPAC_APP_LAVAMD) ? 1 : 0;
+  p.staged = r.app == HPAC_APP_LAVAMD ? 1 : 0;
   p.barrier_eval = (r.flags & HPAC_REGION_BARRIER_IN_EVALUATE) ? 1 : 0;
   p.accumulate = (r.flags & HPAC_REGION_STORE_ACCUMULATE) ? 1 : 0;
   p.paths = launch ? launch->paths : nullptr;
@@ -334,7 +344,25 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
   pr.empty = (te == tb) || n == 0;
 
   // ---- B200 engine limits ------------------------------------------------
-  if (!per_team) {
+  if (r.app == HPAC_APP_LAVAMD) {
+    const long long boxes = (long long)r.lavamd_boxes1d * r.lavamd_boxes1d * r.lavamd_boxes1d;
+    if (!per_team)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "LavaMD runs one box per team (per-team mapping)");
+    if (r.lavamd_particles != g->threads_per_team)
+      return fail(err, el, HPAC_ERR_CONFIG,
+                  "lavamd: particles per box (%d) must equal threads_per_team (%d)",
+                  r.lavamd_particles, g->threads_per_team);
+    if (n > boxes)
+      return fail(err, el, HPAC_ERR_CONFIG, "lavamd: %lld items exceed %lld boxes", (long long)n,
+                  boxes);
+    if (g->threads_per_team > 1024)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED, "threads_per_team > 1024 is not supported");
+    p.per_team = 1;
+    pr.kind = 0;
+    pr.block = p.tpt;
+    pr.nblocks = te - tb;
+    pr.smem = engine_thread_smem(p);
+  } else if (!per_team) {
     if (r.app == HPAC_APP_BINOMIAL)
       return fail(err, el, HPAC_ERR_UNSUPPORTED,
                   "binomial region runs under per-team mapping (bench/run.hpp:44)");
@@ -582,6 +610,14 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
       in_bytes = nn * 40;
       out_bytes = r.out ? nn * 8 : 0;
       break;
+    case HPAC_APP_LAVAMD: {
+      const size_t parts = (size_t)r.lavamd_boxes1d * r.lavamd_boxes1d * r.lavamd_boxes1d *
+                           (size_t)r.lavamd_particles;
+      in_bytes = parts * 32;   // rv (v, x, y, z) of every box (neighbours)
+      tab_bytes = parts * 8;   // qv
+      out_bytes = parts * 32;  // fv (accumulated in place)
+      break;
+    }
     case HPAC_APP_KMEANS:
       in_bytes = nn * r.kmeans_dims * 8;
       cen_bytes = (size_t)r.kmeans_k * r.kmeans_dims * 8;

@@ -205,6 +205,9 @@ class Region:
     binomial_put: int = 1
     kmeans_dims: int = 2
     kmeans_k: int = 8
+    lavamd_boxes1d: int = 0
+    lavamd_particles: int = 0
+    lavamd_alpha: float = 0.5
     seed: int = 0
     inputs: object = None
     table_out: object = None
@@ -219,6 +222,8 @@ class Region:
         r.synthetic_profile, r.binomial_steps = self.synthetic_profile, self.binomial_steps
         r.binomial_american, r.binomial_put = self.binomial_american, self.binomial_put
         r.kmeans_dims, r.kmeans_k, r.seed = self.kmeans_dims, self.kmeans_k, self.seed
+        r.lavamd_boxes1d, r.lavamd_particles = self.lavamd_boxes1d, self.lavamd_particles
+        r.lavamd_alpha = self.lavamd_alpha
         r.in_ = _ptr(self.inputs)
         r.table_out = _ptr(self.table_out)
         r.encounters = _ptr(self.encounters)
@@ -262,6 +267,22 @@ def kmeans_region(points, centroids, labels, distances=None, fast_math=False):
     return Region(abi.APP_KMEANS, d, k, abi.REGION_KMEANS_FAST_MATH if fast_math else 0,
                   kmeans_dims=d, kmeans_k=k, inputs=points, centroids=centroids, labels=labels,
                   out=distances)
+
+
+def lavamd_region(rv, qv, fv, boxes1d, particles, alpha=0.5):
+    """LavaMD (Rodinia lavaMD restated): item = home box,
+    lane = home particle, encounter = neighbour box; fv accumulates."""
+    return Region(abi.APP_LAVAMD, 0, 4, lavamd_boxes1d=boxes1d, lavamd_particles=particles,
+                  lavamd_alpha=alpha, inputs=rv, table_out=qv, out=fv)
+
+
+def make_lavamd(boxes1d, particles, seed):
+    n = boxes1d ** 3 * particles
+    rv = np.empty((n, 4))
+    qv = np.empty(n)
+    if abi.lib().hpac_make_lavamd(boxes1d, particles, seed, rv.ctypes.data, qv.ctypes.data):
+        raise ConfigError("make_lavamd: bad arguments")
+    return rv, qv
 
 
 # ---- launch ----------------------------------------------------------------
