@@ -25,8 +25,10 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
   }
   double d1 = (log(spot / strike) + (rate + 0.5 * vol * vol) * mat) / sst;
   double d2 = d1 - sst;
-  double n1 = 0.5 * erfc(-d1 / 1.4142135623730951);
-  double n2 = 0.5 * erfc(-d2 / 1.4142135623730951);
+  // norm_cdf(x) = erfc(-x/sqrt2)/2 (blackscholes.hpp:21); the division by
+  // sqrt2 is a multiplication by -1/sqrt2 here (<= 1 ulp in the argument)
+  double n1 = 0.5 * erfc(d1 * -0.70710678118654752440);
+  double n2 = 0.5 * erfc(d2 * -0.70710678118654752440);
   price = spot * n1 - disc_strike * n2;
   return true;
 }

@@ -450,7 +450,7 @@ static cudaError_t launch_tech(const EngineParams& p, int nblocks, size_t smem,
     k<<<nblocks, p.tpt, smem, st>>>(p);                                                 \
     return cudaGetLastError();                                                          \
   }
-  if (TECH == HPAC_TECH_TAF) {
+  if constexpr (TECH == HPAC_TECH_TAF) {
     switch (hreg) {
       case 1: HPAC_LAUNCH(1);
       case 2: HPAC_LAUNCH(2);

@@ -1,0 +1,102 @@
+"""The streaming per-thread engine (csrc/engine_stream.cu: bulk-TMA staged
+input tiles) against the generic per-thread engine (HPAC_ENGINE=thread) and
+the oracle, on ragged shapes the C1 grid never exercises: partial last
+tiles (per-thread fallback loads), logical warps narrower than 32, teams of
+32..256 threads, every decision level, TAF and perforation."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2308_16877_b200 import engine as E
+from gpu_util import dev
+
+pytestmark = pytest.mark.gpu
+
+STAT_FIELDS = ["total_invocations", "approx_invocations", "divergent_warp_steps",
+               "total_warp_steps", "resident_warps"]
+
+
+def _run(grid, n, d_opts, spec_fn, engine=None):
+    out = torch.full((n,), -1.0, dtype=torch.float64, device="cuda")
+    paths = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    old = os.environ.pop("HPAC_ENGINE", None)
+    if engine:
+        os.environ["HPAC_ENGINE"] = engine
+    try:
+        lr = E.run_region(grid, n, 0, E.blackscholes_region(d_opts, out), spec_fn(), paths=paths)
+    finally:
+        os.environ.pop("HPAC_ENGINE", None)
+        if old is not None:
+            os.environ["HPAC_ENGINE"] = old
+    return lr, out.cpu().numpy(), paths.cpu().numpy()
+
+
+SHAPES = [  # (num_teams, tpt, ws, ipt, n)
+    (37, 64, 32, 5, 37 * 64 * 5 - 17),
+    (16, 32, 8, 7, 16 * 32 * 7 - 1),
+    (9, 128, 16, 4, 9 * 128 * 3 + 65),
+    (5, 256, 32, 3, 5 * 256 * 3 - 300),
+    (64, 64, 4, 16, 64 * 64 * 16),
+]
+SPECS = [
+    lambda: None,
+    lambda: E.taf(5, 1, 0.5, "thread"),
+    lambda: E.taf(3, 4, 0.05, "warp"),
+    lambda: E.taf(2, 8, float("inf"), "team"),
+    lambda: E.taf(8, 2, 0.3, "thread"),
+    lambda: E.perfo("small", 3),
+    lambda: E.perfo("large", 2, level="warp"),
+    lambda: E.perfo("fini", 30),
+    lambda: E.perfo("random", 40, seed=9, level="team"),
+    lambda: E.perfo("herded_large", 3),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("si", range(len(SPECS)))
+def test_stream_engine_equals_generic_engine(shape, si):
+    teams, tpt, ws, ipt, n = shape
+    opts = E.make_bs_portfolio(n, 11)
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    a = _run(grid, n, d_opts, SPECS[si])
+    b = _run(grid, n, d_opts, SPECS[si], engine="thread")
+    for f in STAT_FIELDS:
+        assert a[0].stats[f] == b[0].stats[f], f
+    assert np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("si", [1, 2, 3, 6, 8])
+def test_stream_engine_vs_oracle_ragged(si):
+    teams, tpt, ws, ipt, n = SHAPES[0]
+    opts = E.make_bs_portfolio(n, 5)
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    _, exact, _ = _run(grid, n, d_opts, lambda: None)
+    lr, g_out, g_paths = _run(grid, n, d_opts, SPECS[si])
+    o_out = np.full(n, -1.0)
+    o_paths = np.zeros(n, np.uint8)
+    rc, st, msg = oracle.oracle_run(grid, n, 0, E.table_region(opts, exact.reshape(n, 1), o_out),
+                                    SPECS[si](), o_paths)
+    assert rc == 0, msg
+    for f in STAT_FIELDS:
+        assert lr.stats[f] == getattr(st, f), f
+    assert np.array_equal(g_paths, o_paths)
+    assert np.array_equal(g_out, o_out)
+
+
+def test_stream_engine_misaligned_input_falls_back():
+    # a view starting 8 bytes into the buffer defeats the 16-byte bulk-copy
+    # alignment; the engine must take per-thread loads and stay exact
+    n = 32 * 64 * 4
+    opts = E.make_bs_portfolio(n + 1, 3)
+    buf = torch.from_numpy(np.concatenate([[0.0], opts.reshape(-1)])).cuda()
+    d_view = buf[1:].view(n + 1, 5)[:n]
+    grid = E.GridConfig(32, 64, 32, 4)
+    a = _run(grid, n, d_view, lambda: E.taf(5, 1, 0.5))
+    b = _run(grid, n, dev(opts[:n]), lambda: E.taf(5, 1, 0.5))
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
