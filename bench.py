@@ -41,6 +41,10 @@ WORKLOADS = {
     "blackscholes": dict(
         name="blackscholes-4M-taf-h5", benchmark="blackscholes", n=1 << 22, ipt=16,
         directive="memo(out:5:1:0.5)", spec=("taf", 5, 1, 0.5, "thread"), unit="options/s"),
+    "lavamd": dict(
+        name="lavamd-64^3-boxes-x-128-taf-warp", benchmark="lavamd", boxes1d=64, particles=128, ipt=1,
+        directive="memo(out:3:8:0.1) level(warp)", spec=("taf", 3, 8, 0.1, "warp"),
+        compare_levels=("thread", "team"), unit="particles/s"),
     "kmeans": dict(
         name="kmeans-16M-x-32-x-64-perfo-small", benchmark="kmeans", n=1 << 24, dims=32, k=64,
         ipt=4, directive="perfo(small:2)", spec=("perfo", "small", 2), unit="point-iterations/s"),
@@ -48,12 +52,37 @@ WORKLOADS = {
 
 # Algorithmic work per item: binomial lattice FP64 flops
 # per evaluated option = 5 per node x N(N+1)/2 nodes.
+def lava_neighbour_counts(boxes, b1):
+    """Neighbour boxes (incl. self) of each home box in a b1^3 grid."""
+    import numpy as np
+    b = np.asarray(boxes)
+    c = np.ones_like(b)
+    for coord in (b % b1, (b // b1) % b1, b // (b1 * b1)):
+        c = c * (3 - (coord == 0) - (coord == b1 - 1))
+    return c
+
+
+def lava_cpu_scale(m, b1):
+    """Boxes 0..m-1 sit on the grid boundary (fewer neighbours): factor that
+    converts their particle rate to the b1^3 system's average work/particle."""
+    import numpy as np
+    sample = lava_neighbour_counts(np.arange(m), b1).mean()
+    full = ((2 * 2 + (b1 - 2) * 3) / b1) ** 3
+    return sample / full
+
+
 def binomial_flops(N):
     return 5.0 * N * (N + 1) / 2.0
 
 
 def kmeans_flops(d, k):
     return 3.0 * d * k + k  # sub, mul, add per (c, d) + sqrt per centroid
+
+
+# LavaMD pair term (apps.cuh AppLavaMD::eval): dot 5, r2 2, exponent arg 1,
+# exp 30 (reduction 5, degree-12 Horner 24, scale 1), q*vij 1, 2qv 1, fv 1,
+# d 3, f 6 = 50 FP64 flops per particle pair
+LAVAMD_PAIR_FLOPS = 50.0
 
 
 # ------------------------------------------------------------------ helpers
@@ -156,9 +185,11 @@ def reference_arm(args, wl):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    lib = oracle.ref()
+    kind = "reference"
+    if wl["benchmark"] != "lavamd":
+        oracle.ref()
     cores = os.cpu_count() or 1
-    n = wl["n"]
+    n = wl.get("n")
     if wl["benchmark"] == "binomial":
         opts = E.make_binomial_portfolio(n, 42)
         grid, mapping = E.resolve_grid("binomial", n, items_per_thread=wl["ipt"])
@@ -190,6 +221,25 @@ def reference_arm(args, wl):
             rc, st, msg = oracle.ref_run(g, per, 0, E.blackscholes_region(sub, out), make_spec(E, wl["spec"]))
             assert rc == 0, msg
             return per
+    elif wl["benchmark"] == "lavamd":
+        # LavaMD is not in the reference: the reference arm
+        # runs our CPU restatement (oracle port) of the same region
+        b1, P = wl["boxes1d"], wl["particles"]
+        rv, qv = E.make_lavamd(b1, P, 42)
+        per = 16  # home boxes per worker and step
+        kind = "port"
+        sample_desc = f"{cores} threads x {per} home boxes of the {b1}^3 system (x{P} particles), oracle port"
+
+        scale = lava_cpu_scale(per, b1)
+        sample_desc += f" (home boxes 0..{per - 1}; rate scaled x{scale:.3f} to the {b1}^3 mean neighbour count)"
+
+        def work(worker, step):
+            fv = np.zeros((b1 ** 3 * P, 4))
+            g = E.GridConfig(per, P, 32, 1)
+            rc, st, msg = oracle.oracle_run(g, per, 1, E.lavamd_region(rv, qv, fv, b1, P),
+                                            make_spec(E, wl["spec"]))
+            assert rc == 0, msg
+            return per * P * scale
     else:
         d, k = wl["dims"], wl["k"]
         per = 1 << 12
@@ -226,7 +276,7 @@ def reference_arm(args, wl):
         "ms_per_step": dt / max(1, args.steps) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["name"], "directive": wl["directive"]},
-        "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": kind,
                          "sample": sample_desc},
         "e2e": {"value": value, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -267,6 +317,19 @@ def cpu_baseline_sample(wl, opts, grid):
                              make_spec(E, wl["spec"]))
         items = m
         desc = f"first {m} options, 1024 teams x 64 x ipt 16, 1 thread"
+    elif wl["benchmark"] == "lavamd":
+        # not in the reference: our oracle restatement
+        runner, kind = oracle.oracle_run, "port"
+        rv, qv = opts
+        b1, P = wl["boxes1d"], wl["particles"]
+        m = 96  # home boxes 0..95 of the 64^3 system, all 27-neighbourhoods
+        fv = np.zeros((b1 ** 3 * P, 4))
+        rc, st, msg = runner(E.GridConfig(m, P, 32, 1), m, 1, E.lavamd_region(rv, qv, fv, b1, P),
+                             make_spec(E, wl["spec"]))
+        scale = lava_cpu_scale(m, b1)
+        items = m * P * scale
+        desc = (f"home boxes 0..{m - 1} of the {b1}^3 system ({m * P} particles), oracle port, 1 thread; "
+                f"rate scaled x{scale:.3f} to the {b1}^3 mean neighbour count")
     else:
         m = 1 << 14
         pts = np.ascontiguousarray(opts[0][:m])
@@ -294,7 +357,7 @@ def our_arm(args, wl):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    n = wl["n"]
+    n = wl.get("n")
     spec = make_spec(E, wl["spec"])
 
     # ---- inputs (synthetic, seeded; each rank its own shard of a ws*n job)
@@ -321,6 +384,21 @@ def our_arm(args, wl):
         flops_item = None
         bound = "hbm"
         cpu_inputs = opts
+    elif wl["benchmark"] == "lavamd":
+        b1, P = wl["boxes1d"], wl["particles"]
+        n = b1 ** 3  # engine items = home boxes; metric items = particles
+        rv, qv = E.make_lavamd(b1, P, seed)
+        grid, mapping = E.resolve_grid("lavamd", n, items_per_thread=wl["ipt"])
+        d_rv = torch.from_numpy(rv).to(dev)
+        d_qv = torch.from_numpy(qv).to(dev)
+        out_exact = torch.zeros((n * P, 4), dtype=torch.float64, device=dev)
+        out = torch.zeros((n * P, 4), dtype=torch.float64, device=dev)
+        mk = lambda o, s=None: E.lavamd_region(d_rv, d_qv, o, b1, P)
+        h2d_bytes, d2h_bytes = n * P * (32 + 8 + 32), n * P * 32
+        flops_item = LAVAMD_PAIR_FLOPS * P  # per evaluated (particle, neighbour box)
+        bound = "fp64"
+        cpu_inputs = (rv, qv)
+        per_item = P
     else:
         d, k = wl["dims"], wl["k"]
         pts = E.make_blobs(n, d, k, seed, 8.0)
@@ -336,6 +414,9 @@ def our_arm(args, wl):
         bound = "fp64"
         cpu_inputs = (pts, cents)
 
+    if wl["benchmark"] != "lavamd":
+        per_item = 1  # metric items per engine item (LavaMD: particles per box)
+
     # L2 flush buffer (> 126 MB L2), written between timed iterations
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
@@ -349,6 +430,8 @@ def our_arm(args, wl):
             # L2 flush (256 MB write) is enqueued first and left running, so the
             # host-side launch of the region overlaps it; the region kernel is
             # bracketed by the library's CUDA events on this stream (kernel_ms)
+            if wl["benchmark"] == "lavamd":
+                target.zero_()  # fv accumulates (Rodinia fv += ...)
             flush.zero_()
             E.run_region(grid, n, mapping, mk(target), sp, stream=stream, synchronous=False)
             torch.cuda.synchronize()
@@ -374,10 +457,10 @@ def our_arm(args, wl):
     # quality loss (application metric) vs the exact run
     if wl["benchmark"] == "kmeans":
         quality = {"mcr": E.mcr(out_exact, out)}
-        qv = quality["mcr"]
+        qval = quality["mcr"]
     else:
         quality = {"mape": E.mape(out_exact, out)}
-        qv = quality["mape"]
+        qval = quality["mape"]
 
     t_apx = sum(ts_apx)
     t_exact = sum(ts_exact)
@@ -385,8 +468,24 @@ def our_arm(args, wl):
         t = torch.tensor([t_apx, t_exact], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_apx, t_exact = t.tolist()
-    value = ws * n * args.steps / (t_apx * 1e-3)
-    exact_value = ws * n * args.steps / (t_exact * 1e-3)
+    value = ws * n * per_item * args.steps / (t_apx * 1e-3)
+    exact_value = ws * n * per_item * args.steps / (t_exact * 1e-3)
+
+    # ---- decision granularity comparison (C4: warp vs team, + thread)
+    levels = None
+    if wl.get("compare_levels"):
+        levels = {wl["spec"][-1]: {"speedup_vs_exact": t_exact / t_apx, "quality": qval,
+                                   "approx_rate": st_apx["approx_invocations"] / max(1, st_apx["total_invocations"]),
+                                   "divergent_fraction": st_apx["divergent_warp_steps"] / max(1, st_apx["total_warp_steps"])}}
+        for lv in wl["compare_levels"]:
+            sp_l = make_spec(E, tuple(wl["spec"][:-1]) + (lv,))
+            o_l = torch.zeros_like(out)
+            ts_l, st_l = timed_run(o_l, sp_l, max(1, args.steps // 2), 1)
+            levels[lv] = {"speedup_vs_exact": (t_exact / len(ts_exact)) / (sum(ts_l) / len(ts_l)),
+                          "quality": E.mape(out_exact, o_l),
+                          "approx_rate": st_l["approx_invocations"] / max(1, st_l["total_invocations"]),
+                          "divergent_fraction": st_l["divergent_warp_steps"] / max(1, st_l["total_warp_steps"])}
+            del o_l
     ms_per_step = t_apx / args.steps
 
     # ---- end to end through the C-ABI with pinned host buffers
@@ -396,6 +495,11 @@ def our_arm(args, wl):
             h_in = torch.from_numpy(pts).pin_memory()
             h_lab = torch.zeros(n, dtype=torch.int32).pin_memory()
             hreg = E.kmeans_region(h_in.numpy(), cents, h_lab.numpy())
+        elif wl["benchmark"] == "lavamd":
+            h_rv = torch.from_numpy(rv).pin_memory()
+            h_qv = torch.from_numpy(qv).pin_memory()
+            h_fv = torch.zeros((n * P, 4), dtype=torch.float64).pin_memory()
+            hreg = E.lavamd_region(h_rv.numpy(), h_qv.numpy(), h_fv.numpy(), b1, P)
         else:
             h_in = torch.from_numpy(cpu_inputs).pin_memory()
             h_out = torch.zeros(n, dtype=torch.float64).pin_memory()
@@ -412,7 +516,7 @@ def our_arm(args, wl):
             t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_t = t.item()
-        e2e = {"value": ws * n * args.e2e_steps / e2e_t, "unit": wl["unit"],
+        e2e = {"value": ws * n * per_item * args.e2e_steps / e2e_t, "unit": wl["unit"],
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
                "steps": args.e2e_steps}
 
@@ -429,7 +533,9 @@ def our_arm(args, wl):
         fp = C.c_double()
         abi.lib().hpac_probe_fp64_peak(C.byref(fp))
         evaluated = st_apx["total_invocations"] - st_apx["approx_invocations"]
-        per_item_lanes = grid.threads_per_team if mapping == 1 else 1
+        # per-team mapping: the team's lanes evaluate one item redundantly,
+        # except LavaMD where each lane is its own particle
+        per_item_lanes = grid.threads_per_team if (mapping == 1 and per_item == 1) else 1
         evaluated_items = evaluated / per_item_lanes
         achieved = evaluated_items * flops_item / (avg_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp.value, "unit": "TFLOP/s",
@@ -464,12 +570,16 @@ def our_arm(args, wl):
             cpu = {"value": None, "unit": wl["unit"], "cores": 1, "kind": "reference",
                    "sample": f"failed: {exc}"}
 
+    if levels:
+        extra_levels = {"decision_levels": levels}
+    else:
+        extra_levels = {}
     line = {
         "metric": METRIC, "value": value, "unit": wl["unit"], "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generators, seed 42 + rank)",
-        "config": {"workload": wl["name"], "n_per_gpu": n, "directive": wl["directive"],
+        "config": {"workload": wl["name"], "n_per_gpu": n * per_item, "directive": wl["directive"],
                    "grid": {"num_teams": grid.num_teams, "threads_per_team": grid.threads_per_team,
                             "warp_size": grid.warp_size, "items_per_thread": grid.items_per_thread},
                    "mapping": "per-team" if mapping == 1 else "per-thread",
@@ -477,10 +587,11 @@ def our_arm(args, wl):
                    "parallelism": f"dp{ws} (independent shards)"},
         "speedup_vs_exact": value / exact_value,
         "exact_value": exact_value,
-        "quality": quality, "quality_ok": bool(qv <= 0.01),
+        "quality": quality, "quality_ok": bool(qval <= 0.01),
         "approx_rate": st_apx["approx_invocations"] / max(1, st_apx["total_invocations"]),
+        "divergent_fraction": st_apx["divergent_warp_steps"] / max(1, st_apx["total_warp_steps"]),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": args.steps, "clocks": clk,
+        "gpu_launches": args.steps, "clocks": clk, **extra_levels,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

@@ -387,23 +387,26 @@ typedef struct {
 } region_view;
 
 /* LavaMD (extension; the framework's restatement of Rodinia lavaMD, SURVEY
-   Appendix C): the same fixed round-to-nearest exp as the device code. */
+   Appendix C; Rodinia is not under /root/reference, so parity is unpinned):
+   exp as Cody-Waite reduction + degree-12 Taylor in fma() Horner form, the
+   same sequence as the device code (fma() is exactly rounded on both). */
 static double lava_exp(double x) {
   const double kd = rint(x * 1.4426950408889634);
-  const double r = (x + -(kd * 0x1.62e42fee00000p-1)) + -(kd * 0x1.a39ef35793c76p-33);
+  double r = fma(-kd, 0x1.62e42fee00000p-1, x);
+  r = fma(-kd, 0x1.a39ef35793c76p-33, r);
   double s = 1.0 / 479001600.0;
-  s = s * r + 1.0 / 39916800.0;
-  s = s * r + 1.0 / 3628800.0;
-  s = s * r + 1.0 / 362880.0;
-  s = s * r + 1.0 / 40320.0;
-  s = s * r + 1.0 / 5040.0;
-  s = s * r + 1.0 / 720.0;
-  s = s * r + 1.0 / 120.0;
-  s = s * r + 1.0 / 24.0;
-  s = s * r + 1.0 / 6.0;
-  s = s * r + 0.5;
-  s = s * r + 1.0;
-  s = s * r + 1.0;
+  s = fma(s, r, 1.0 / 39916800.0);
+  s = fma(s, r, 1.0 / 3628800.0);
+  s = fma(s, r, 1.0 / 362880.0);
+  s = fma(s, r, 1.0 / 40320.0);
+  s = fma(s, r, 1.0 / 5040.0);
+  s = fma(s, r, 1.0 / 720.0);
+  s = fma(s, r, 1.0 / 120.0);
+  s = fma(s, r, 1.0 / 24.0);
+  s = fma(s, r, 1.0 / 6.0);
+  s = fma(s, r, 0.5);
+  s = fma(s, r, 1.0);
+  s = fma(s, r, 1.0);
   return ldexp(s, (int)kd);
 }
 
@@ -449,7 +452,7 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
   switch (r->app) {
     case HPAC_APP_LAVAMD: {
       const int P = r->lavamd_particles;
-      const double a2 = 2.0 * r->lavamd_alpha * r->lavamd_alpha;
+      const double na2 = -(2.0 * r->lavamd_alpha * r->lavamd_alpha);
       int64_t nb[27];
       lava_neighbours(idx, r->lavamd_boxes1d, nb);
       const int64_t b = nb[round];
@@ -458,14 +461,17 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
       for (int j = 0; j < P; ++j) {
         const double* o2 = r->in + (b * P + j) * 4;
         const double q = r->table_out[b * P + j];
-        const double dot = (me[1] * o2[1] + me[2] * o2[2]) + me[3] * o2[3];
+        /* Rodinia lavaMD pair term: r2 = rA.v + rB.v - dot(rA, rB),
+           vij = exp(-a2 r2), f += qB (vij, 2 vij (rA - rB)); FMA form */
+        const double dot = fma(me[3], o2[3], fma(me[2], o2[2], me[1] * o2[1]));
         const double r2 = (me[0] + o2[0]) - dot;
-        const double vij = lava_exp(-(a2 * r2));
-        const double fs = 2.0 * vij;
-        fv = fv + q * vij;
-        fx = fx + q * (fs * (me[1] - o2[1]));
-        fy = fy + q * (fs * (me[2] - o2[2]));
-        fz = fz + q * (fs * (me[3] - o2[3]));
+        const double vij = lava_exp(na2 * r2);
+        const double qv = q * vij;
+        const double t = qv + qv;
+        fv = fv + qv;
+        fx = fma(t, me[1] - o2[1], fx);
+        fy = fma(t, me[2] - o2[2], fy);
+        fz = fma(t, me[3] - o2[3], fz);
       }
       out[0] = fv;
       out[1] = fx;

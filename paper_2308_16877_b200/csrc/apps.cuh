@@ -37,10 +37,12 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
 // engine.hpp:29; 1 by default) and a per-round staging step executed by
 // every thread of the team outside the approximated region.
 struct AppBase {
+  // occupancy hint for the 256-thread engine instantiation (launch bounds)
+  static constexpr int MIN_BLOCKS_256 = 1;
   __device__ static int encounters(const EngineParams& p, int64_t idx) {
     return p.region.encounters ? p.region.encounters[idx] : 1;
   }
-  __device__ static void round_begin(const EngineParams&, int64_t, int, double*, bool) {}
+  __device__ static void round_begin(const EngineParams&, int64_t, int, double*, bool, bool) {}
 };
 
 // Generic pure region over a work index (HPAC_APP_TABLE): load_input reads
@@ -212,34 +214,42 @@ struct AppKmeans : AppBase {
 // lane's particle: out = (v, x, y, z) accumulated into fv. Neighbour
 // particles are staged in shared memory by the whole team OUTSIDE the
 // region (round_begin), so thread/warp decisions never skip a barrier.
-// exp() is a fixed round-to-nearest sequence shared with the oracle, so the
-// contributions (and TAF decisions on them) are bit-identical to the CPU.
+// exp() is a fixed sequence of correctly rounded operations and fused
+// multiply-adds (fma() is exactly rounded on both sides), shared with the
+// oracle, so the contributions (and TAF decisions on them) are bit-identical
+// to the CPU restatement.
+// Coefficients live in constant memory on the device so the DFMAs take them
+// as c[bank][offset] operands (64-bit immediates would otherwise be
+// re-materialised with two integer moves per use inside the pair loop).
+static __constant__ double kLavaExpC[16] = {
+    1.4426950408889634, 0x1.62e42fee00000p-1, 0x1.a39ef35793c76p-33,
+    1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
+    1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0, 0x1.8p52};
+
 __host__ __device__ __forceinline__ double lava_exp(double x) {
 #ifdef __CUDA_ARCH__
-#define LMUL __dmul_rn
-#define LADD __dadd_rn
+  const double* c = kLavaExpC;
+  // rint(x*log2e) via the 1.5*2^52 shifter (round-to-nearest-even, |t| < 2^51)
+  const double kd = __dsub_rn(__dadd_rn(__dmul_rn(x, c[0]), c[15]), c[15]);
 #else
-#define LMUL(a, b) ((a) * (b))
-#define LADD(a, b) ((a) + (b))
+  static const double c[16] = {
+      1.4426950408889634, 0x1.62e42fee00000p-1, 0x1.a39ef35793c76p-33,
+      1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
+      1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0, 0x1.8p52};
+  const double kd = rint(x * c[0]);
 #endif
-  const double kd = rint(LMUL(x, 1.4426950408889634));
-  const double r = LADD(LADD(x, -LMUL(kd, 0x1.62e42fee00000p-1)), -LMUL(kd, 0x1.a39ef35793c76p-33));
-  double s = 1.0 / 479001600.0;  // 1/12!
-  s = LADD(LMUL(s, r), 1.0 / 39916800.0);
-  s = LADD(LMUL(s, r), 1.0 / 3628800.0);
-  s = LADD(LMUL(s, r), 1.0 / 362880.0);
-  s = LADD(LMUL(s, r), 1.0 / 40320.0);
-  s = LADD(LMUL(s, r), 1.0 / 5040.0);
-  s = LADD(LMUL(s, r), 1.0 / 720.0);
-  s = LADD(LMUL(s, r), 1.0 / 120.0);
-  s = LADD(LMUL(s, r), 1.0 / 24.0);
-  s = LADD(LMUL(s, r), 1.0 / 6.0);
-  s = LADD(LMUL(s, r), 0.5);
-  s = LADD(LMUL(s, r), 1.0);
-  s = LADD(LMUL(s, r), 1.0);
-  return ldexp(s, (int)kd);
-#undef LMUL
-#undef LADD
+  double r = fma(-kd, c[1], x);
+  r = fma(-kd, c[2], r);
+  double s = c[3];  // 1/12!
+#pragma unroll
+  for (int i = 4; i <= 14; ++i) s = fma(s, r, c[i]);
+  s = fma(s, r, 1.0);
+  const int k = (int)kd;
+#ifdef __CUDA_ARCH__
+  // exact power-of-two scaling == ldexp while 2^k is a normal double
+  if (k > -1023 && k < 1024) return s * __longlong_as_double((long long)(k + 1023) << 52);
+#endif
+  return ldexp(s, k);
 }
 
 __host__ __device__ __forceinline__ int lava_neighbours(int64_t box, int b1, int64_t* nb) {
@@ -259,7 +269,59 @@ __host__ __device__ __forceinline__ int lava_neighbours(int64_t box, int b1, int
   return c;
 }
 
+// the r-th neighbour box of `box` in lava_neighbours order (no local array)
+__host__ __device__ __forceinline__ int64_t lava_neighbour_at(int64_t box, int b1, int r) {
+  if (r == 0) return box;
+  const int bx = (int)(box % b1), by = (int)((box / b1) % b1), bz = (int)(box / ((int64_t)b1 * b1));
+  int c = 1;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (!dx && !dy && !dz) continue;
+        const int x = bx + dx, y = by + dy, z = bz + dz;
+        if (x < 0 || y < 0 || z < 0 || x >= b1 || y >= b1 || z >= b1) continue;
+        if (c == r) return ((int64_t)z * b1 + y) * b1 + x;
+        ++c;
+      }
+  return -1;
+}
+
+// The pair loop over a staged neighbour box, kept out of line so its register
+// allocation (and the code ptxas generates for it) does not depend on the
+// engine state live around it (TAF windows, votes): the exact and the
+// approximate kernels run the identical loop.
+static __device__ __noinline__ double4 lava_box_contribution(const double* rv_home, const double* s, int P,
+                                                      double na2) {
+  const double4 me = *reinterpret_cast<const double4*>(rv_home);
+  double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+#ifndef HPAC_LAVA_UNROLL
+#define HPAC_LAVA_UNROLL 1  // measured: 1 (32.7 ms) < 4 (35.5) < 2 (36.5) at 32^3
+#endif
+  constexpr int kUnroll = HPAC_LAVA_UNROLL;
+#pragma unroll kUnroll
+  for (int j = 0; j < P; ++j) {
+    const double2 b01 = *reinterpret_cast<const double2*>(s + j * 4);
+    const double2 b23 = *reinterpret_cast<const double2*>(s + j * 4 + 2);
+    const double q = s[P * 4 + j];
+    const double dot = fma(me.w, b23.y, fma(me.z, b23.x, __dmul_rn(me.y, b01.y)));
+    const double r2 = __dsub_rn(__dadd_rn(me.x, b01.x), dot);
+    const double vij = lava_exp(__dmul_rn(na2, r2));
+    const double qv = __dmul_rn(q, vij);
+    const double t = __dadd_rn(qv, qv);
+    fv = __dadd_rn(fv, qv);
+    fx = fma(t, __dsub_rn(me.y, b01.y), fx);
+    fy = fma(t, __dsub_rn(me.z, b23.x), fy);
+    fz = fma(t, __dsub_rn(me.w, b23.y), fz);
+  }
+  return make_double4(fv, fx, fy, fz);
+}
+
 struct AppLavaMD : AppBase {
+  // FP64-latency-bound pair loop: keep >= 24 warps per SM (<= 85 registers)
+#ifndef HPAC_LAVA_MINB
+#define HPAC_LAVA_MINB 3
+#endif
+  static constexpr int MIN_BLOCKS_256 = HPAC_LAVA_MINB;
   static constexpr int IN_MAX = 1;
   static constexpr int OUT_MAX = 4;
   __device__ static void init(const EngineParams&, double*) {}
@@ -267,45 +329,36 @@ struct AppLavaMD : AppBase {
     return lava_neighbours(idx, p.region.lavamd_boxes1d, nullptr);
   }
   // stage neighbour box `round` of home box idx: rv (4) + qv (1) per particle
+  // `need`: this thread evaluates in this round. The first barrier also
+  // retires the previous round's readers of s; nothing is staged when no
+  // thread of the team evaluates (team-uniform result of the barrier).
   __device__ static void round_begin(const EngineParams& p, int64_t idx, int round, double* s,
-                                     bool valid) {
-    __syncthreads();  // previous round's evaluations are done with s
+                                     bool valid, bool need) {
+    if (!__syncthreads_or(need)) return;
     if (valid) {
-      int64_t nb[27];
-      const int c = lava_neighbours(idx, p.region.lavamd_boxes1d, nb);
-      if (round < c) {
+      const int64_t b = lava_neighbour_at(idx, p.region.lavamd_boxes1d, round);
+      if (b >= 0) {
         const int P = p.region.lavamd_particles;
-        const int64_t b = nb[round];
-        for (int i = threadIdx.x; i < P * 4; i += blockDim.x) s[i] = __ldg(p.region.in + b * P * 4 + i);
+        const double2* src = reinterpret_cast<const double2*>(p.region.in + b * P * 4);
+        double2* dst = reinterpret_cast<double2*>(s);
+        for (int i = threadIdx.x; i < P * 2; i += blockDim.x) dst[i] = __ldg(src + i);
         for (int i = threadIdx.x; i < P; i += blockDim.x) s[P * 4 + i] = __ldg(p.region.table_out + b * P + i);
       }
     }
     __syncthreads();
   }
   __device__ static void load(const EngineParams&, int64_t, double (&)[IN_MAX]) {}
+  // one neighbour box's contribution to the lane's particle (Rodinia
+  // lavaMD kernel body, FMA form restated identically in the oracle)
   __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&)[IN_MAX],
                               double (&out)[OUT_MAX], const double* s, int local, int) {
     const int P = p.region.lavamd_particles;
-    const double a2 = __dmul_rn(__dmul_rn(2.0, p.region.lavamd_alpha), p.region.lavamd_alpha);
-    const double* me = p.region.in + (idx * P + local) * 4;
-    const double av = me[0], ax = me[1], ay = me[2], az = me[3];
-    double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-    for (int j = 0; j < P; ++j) {
-      const double bv = s[j * 4], bx = s[j * 4 + 1], by = s[j * 4 + 2], bz = s[j * 4 + 3];
-      const double q = s[P * 4 + j];
-      const double dot = __dadd_rn(__dadd_rn(__dmul_rn(ax, bx), __dmul_rn(ay, by)), __dmul_rn(az, bz));
-      const double r2 = __dsub_rn(__dadd_rn(av, bv), dot);
-      const double vij = lava_exp(-__dmul_rn(a2, r2));
-      const double fs = __dmul_rn(2.0, vij);
-      fv = __dadd_rn(fv, __dmul_rn(q, vij));
-      fx = __dadd_rn(fx, __dmul_rn(q, __dmul_rn(fs, __dsub_rn(ax, bx))));
-      fy = __dadd_rn(fy, __dmul_rn(q, __dmul_rn(fs, __dsub_rn(ay, by))));
-      fz = __dadd_rn(fz, __dmul_rn(q, __dmul_rn(fs, __dsub_rn(az, bz))));
-    }
-    out[0] = fv;
-    out[1] = fx;
-    out[2] = fy;
-    out[3] = fz;
+    const double na2 = -__dmul_rn(__dmul_rn(2.0, p.region.lavamd_alpha), p.region.lavamd_alpha);
+    const double4 f = lava_box_contribution(p.region.in + (idx * P + local) * 4, s, P, na2);
+    out[0] = f.x;
+    out[1] = f.y;
+    out[2] = f.z;
+    out[3] = f.w;
     return true;
   }
   __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX],

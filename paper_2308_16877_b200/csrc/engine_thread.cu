@@ -43,8 +43,16 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v,
 
 }  // namespace
 
+// TAF window in registers for single-output apps (h <= 8); multi-output
+// windows live in a shared ring [dim][slot][thread] so they hold no
+// registers across the accurate path (LavaMD's pair loop)
+int engine_thread_max_out(int app);
+static inline bool taf_window_in_registers(const EngineParams& p) {
+  return p.taf_h <= 8 && engine_thread_max_out(p.region.app) == 1;
+}
+
 template <class App, int TECH, int HREG, int MAXT>
-__global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams p) {
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) engine_thread_kernel(const EngineParams p) {
   extern __shared__ __align__(16) double smem[];
   constexpr int IN_MAX = App::IN_MAX;
   constexpr int OUT_MAX = App::OUT_MAX;
@@ -71,12 +79,21 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
 
   // ---- TAF state (TafState, taf.hpp:59-163) -------------------------------
   int taf_mode = kTafFilling, taf_rem = 0, taf_count = 0, taf_head = 0;
-  double win[HREG > 0 ? HREG : 1];
+  // TAF window: registers [slot][dim] oldest first for single-output apps
+  // (REGWIN), else a shared ring [dim][slot][thread] of compile-time length
+  // HREG (HREG > 0) or of runtime length p.taf_h (HREG == 0)
+  constexpr bool REGWIN = HREG > 0 && OUT_MAX == 1;
+  constexpr int HW = HREG > 0 ? HREG : 1;
+  double win[REGWIN ? HW : 1][REGWIN ? OUT_MAX : 1];
+  const double taf_t2 = p.taf_thr * p.taf_thr;
+  const double taf_t_lo = taf_t2 * (1.0 - 1e-9) - 1e-27, taf_t_hi = taf_t2 * (1.0 + 1e-9) + 1e-27;
   double last[OUT_MAX];
 #pragma unroll
   for (int d = 0; d < OUT_MAX; ++d) last[d] = 0.0;
 #pragma unroll
-  for (int i = 0; i < (HREG > 0 ? HREG : 1); ++i) win[i] = 0.0;
+  for (int i = 0; i < (REGWIN ? HW : 1); ++i)
+#pragma unroll
+    for (int d = 0; d < (REGWIN ? OUT_MAX : 1); ++d) win[i][d] = 0.0;
   double* ring = smem + p.smem_taf_off;  // [d][slot][tpt] (smem variant)
 
   // ---- iACT per-table bookkeeping (MemoTable, iact.hpp:58-145) -----------
@@ -122,7 +139,6 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
     for (int round = 0; round < rounds; ++round, ++round_ctr) {
       const int buf = round_ctr % 3;
       const bool in_round = active && round < enc;
-      if (p.staged) App::round_begin(p, idx, round, smem + p.smem_scratch_off, active);
 
       // ---- predicate phase (engine.hpp:221-251) ----------------------------
       double in[IN_MAX];
@@ -209,6 +225,12 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
         }
       }
 
+      // ---- team staging outside the region (staged apps: LavaMD). Decisions
+      // come first: they never read the staged data (TAF/perforation), and a
+      // round in which no lane of the team evaluates stages nothing.
+      if (p.staged)
+        App::round_begin(p, idx, round, smem + p.smem_scratch_off, active, in_round && !approx);
+
       // ---- lane execution (engine.hpp:303-347) -----------------------------
       double out[OUT_MAX];
 #pragma unroll
@@ -247,14 +269,14 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
           if (TECH == HPAC_TECH_TAF) {
             // TafState::observe_accurate, taf.hpp:94-108
             bool full;
-            if (HREG > 0) {
+            if constexpr (REGWIN) {
 #pragma unroll
-              for (int i = 0; i + 1 < (HREG > 0 ? HREG : 1); ++i) win[i] = win[i + 1];
-              win[(HREG > 0 ? HREG : 1) - 1] = out[0];
+              for (int i = 0; i + 1 < HW; ++i) win[i][0] = win[i + 1][0];
+              win[HW - 1][0] = out[0];
               if (taf_count < HREG) ++taf_count;
               full = taf_count == HREG;
             } else {
-              const int h = p.taf_h;
+              const int h = HREG > 0 ? HREG : p.taf_h;
               int slot;
               if (taf_count < h) {
                 slot = taf_head + taf_count;
@@ -264,8 +286,9 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
                 slot = taf_head;
                 taf_head = taf_head + 1 == h ? 0 : taf_head + 1;
               }
-              for (int d = 0; d < p.out_dims; ++d)
-                ring[(d * h + slot) * p.tpt + local] = out[d];
+#pragma unroll
+              for (int d = 0; d < OUT_MAX; ++d)
+                if (d < p.out_dims) ring[(d * h + slot) * p.tpt + local] = out[d];
               full = taf_count == h;
             }
 #pragma unroll
@@ -278,11 +301,20 @@ __global__ void __launch_bounds__(MAXT) engine_thread_kernel(const EngineParams 
                 taf_mode = kTafFilling;
               }
             } else if (check) {
-              bool pass;
-              if (HREG > 0) {
-                pass = taf_window_passes<(HREG > 0 ? HREG : 1)>(win, p.taf_thr);
+              // every output dimension must pass (taf.hpp:134-140)
+              bool pass = true;
+              if constexpr (REGWIN) {
+                double col[HW];
+#pragma unroll
+                for (int i = 0; i < HW; ++i) col[i] = win[i][0];
+                pass = taf_window_passes<HW>(col, p.taf_thr);
+              } else if constexpr (HREG > 0) {
+#pragma unroll
+                for (int d = 0; d < OUT_MAX; ++d)
+                  if (d < p.out_dims && pass)
+                    pass = taf_ring_passes_fixed<HW>(ring + d * HW * p.tpt + local, p.tpt, taf_head,
+                                                     p.taf_thr, taf_t_lo, taf_t_hi);
               } else {
-                pass = true;
                 for (int d = 0; d < p.out_dims && pass; ++d)
                   pass = taf_ring_passes(ring + d * p.taf_h * p.tpt + local, p.tpt, p.taf_h,
                                          taf_head, taf_count, p.taf_thr);
@@ -436,8 +468,10 @@ template <class App, int TECH>
 static cudaError_t launch_tech(const EngineParams& p, int nblocks, size_t smem,
                                cudaStream_t st) {
   // TAF: register shift-register window for single-output regions, h <= 8
+  // compile-time window length for h <= 8 (registers for single-output
+  // apps, a fixed-length shared ring otherwise); h > 8: runtime-length ring
   int hreg = 0;
-  if (TECH == HPAC_TECH_TAF && p.out_dims == 1 && p.taf_h <= 8) hreg = p.taf_h;
+  if (TECH == HPAC_TECH_TAF && p.taf_h <= 8) hreg = p.taf_h;
 #define HPAC_LAUNCH(H)                                                                  \
   {                                                                                     \
     auto k = p.tpt <= 256 ? engine_thread_kernel<App, TECH, H, 256>                     \
@@ -482,13 +516,14 @@ size_t engine_thread_smem(EngineParams& p) {
   size_t off = 0;  // in doubles
   p.smem_taf_off = 0;
   p.smem_last_off = 0;
-  if (p.tech == HPAC_TECH_TAF && !(p.out_dims == 1 && p.taf_h <= 8)) {
+  if (p.tech == HPAC_TECH_TAF && !taf_window_in_registers(p)) {
     p.smem_taf_off = (int)off;
     off += (size_t)p.out_dims * p.taf_h * p.tpt;
   }
   p.smem_tab_off = (int)off;
   if (p.tech == HPAC_TECH_IACT)
     off += (size_t)p.tsize * (p.in_dims + p.out_dims) * p.wpt * p.tpw;
+  off = (off + 1) & ~(size_t)1;  // 16-byte aligned scratch (vector staging)
   p.smem_scratch_off = (int)off;
   if (p.region.app == HPAC_APP_KMEANS)
     off += (size_t)p.region.kmeans_k * p.region.kmeans_dims;

@@ -72,7 +72,7 @@ __device__ __forceinline__ int64_t trip_count(int64_t owner, int64_t stride, int
 // rsd, taf.hpp:29-40: two-pass population sigma / |mu|, window order,
 // no contraction, IEEE sqrt/div.
 template <int H>
-__device__ __forceinline__ bool taf_window_passes(const double (&w)[H], double thr) {
+__device__ __forceinline__ bool taf_window_passes_exact(const double (&w)[H], double thr) {
   double mean = 0.0;
 #pragma unroll
   for (int i = 0; i < H; ++i) mean = __dadd_rn(mean, w[i]);
@@ -92,10 +92,48 @@ __device__ __forceinline__ bool taf_window_passes(const double (&w)[H], double t
   return r <= thr;
 }
 
+// reciprocal to ~2^-50 relative: MUFU seed + two Newton steps (no IEEE path)
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Same decision as taf_window_passes_exact, computed first without IEEE
+// division / square root: r^2 ~= ssd / (H mean^2) from an approximate mean.
+// The approximation is within ~1e-14 relative plus ~1e-30 absolute (the
+// mean's last-ulp error feeding ssd) of the exact r^2, so whenever it lies
+// outside thr^2 (1 +- 1e-9) +- 1e-27 the exact test must agree; NaN/inf
+// windows, mean ~ 0 and near-threshold windows take the exact path.
+template <int H>
+__device__ __forceinline__ bool taf_window_passes(const double (&w)[H], double thr) {
+  double sum = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) sum = __dadd_rn(sum, w[i]);
+  const double mean_a = sum * (1.0 / H);
+  double ssd_a = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const double d = w[i] - mean_a;
+    ssd_a = fma(d, d, ssd_a);
+  }
+  const double den = (double)H * mean_a * mean_a;
+  const double r2 = ssd_a * rcp_fast(den);
+  const double t2 = thr * thr;
+  if (den > 1e-290 && den < 1e290) {
+    if (r2 < t2 * (1.0 - 1e-9) - 1e-27) return true;
+    if (r2 > t2 * (1.0 + 1e-9) + 1e-27) return false;
+  }
+  return taf_window_passes_exact<H>(w, thr);
+}
+
 // Same RSD over a strided window in shared memory: w[j*stride] for j in
 // [0, len) in ring order starting at `head` (taf.hpp:82-88).
-__device__ __forceinline__ bool taf_ring_passes(const double* ring, int stride, int h, int head,
-                                                int len, double thr) {
+__device__ __forceinline__ bool taf_ring_passes_exact(const double* ring, int stride, int h,
+                                                      int head, int len, double thr) {
   double mean = 0.0;
   for (int j = 0; j < len; ++j) {
     int slot = head + j;
@@ -117,6 +155,62 @@ __device__ __forceinline__ bool taf_ring_passes(const double* ring, int stride, 
   else
     r = __ddiv_rn(sigma, fabs(mean));
   return r <= thr;
+}
+
+// division-free estimate first, exact RSD near the threshold (see
+// taf_window_passes for the margin argument)
+__device__ __forceinline__ bool taf_ring_passes(const double* ring, int stride, int h, int head,
+                                                int len, double thr) {
+  double sum = 0.0;
+  for (int j = 0; j < len; ++j) {
+    int slot = head + j;
+    if (slot >= h) slot -= h;
+    sum = __dadd_rn(sum, ring[slot * stride]);
+  }
+  const double mean_a = sum * rcp_fast((double)len);
+  double ssd_a = 0.0;
+  for (int j = 0; j < len; ++j) {
+    int slot = head + j;
+    if (slot >= h) slot -= h;
+    const double d = ring[slot * stride] - mean_a;
+    ssd_a = fma(d, d, ssd_a);
+  }
+  const double den = (double)len * mean_a * mean_a;
+  const double r2 = ssd_a * rcp_fast(den);
+  const double t2 = thr * thr;
+  if (den > 1e-290 && den < 1e290) {
+    if (r2 < t2 * (1.0 - 1e-9) - 1e-27) return true;
+    if (r2 > t2 * (1.0 + 1e-9) + 1e-27) return false;
+  }
+  return taf_ring_passes_exact(ring, stride, h, head, len, thr);
+}
+
+// Ring window of compile-time length H, full (count == H, which is the only
+// state a TAF check sees): division-free estimate over the slots in any
+// order, the exact ring-order RSD only near the threshold. t_lo / t_hi are
+// thr^2 (1 -+ 1e-9) -+ 1e-27 (see taf_window_passes).
+template <int H>
+__device__ __forceinline__ bool taf_ring_passes_fixed(const double* ring, int stride, int head,
+                                                      double thr, double t_lo, double t_hi) {
+  double w[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) w[i] = ring[i * stride];
+  double sum = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) sum += w[i];
+  const double mean_a = sum * (1.0 / H);
+  double ssd_a = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const double d = w[i] - mean_a;
+    ssd_a = fma(d, d, ssd_a);
+  }
+  const double den = (double)H * mean_a * mean_a;
+  if (den > 1e-290 && den < 1e290) {
+    if (ssd_a < den * t_lo) return true;
+    if (ssd_a > den * t_hi) return false;
+  }
+  return taf_ring_passes_exact(ring, stride, H, head, H, thr);
 }
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }

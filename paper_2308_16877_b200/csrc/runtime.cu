@@ -359,6 +359,9 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
     if (n > boxes)
       return fail(err, el, HPAC_ERR_CONFIG, "lavamd: %lld items exceed %lld boxes", (long long)n,
                   boxes);
+    if ((reinterpret_cast<uintptr_t>(r.in) & 31) != 0)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED,
+                  "lavamd: rv must be 32-byte aligned (one double4 per particle)");
     if (g->threads_per_team > 1024)
       return fail(err, el, HPAC_ERR_UNSUPPORTED, "threads_per_team > 1024 is not supported");
     p.per_team = 1;
@@ -497,6 +500,9 @@ HPAC_API int hpac_resolve_grid(const char* benchmark, int64_t n, const hpac_grid
       {"synthetic-constant", 16384, 64, 32, 32, HPAC_MAP_PER_THREAD},
       {"synthetic-slow-drift", 16384, 64, 32, 32, HPAC_MAP_PER_THREAD},
       {"synthetic-noise", 16384, 64, 32, 32, HPAC_MAP_PER_THREAD},
+      // extension: one box per team, lane = particle (128 = 4 whole warps;
+      // grid.hpp:27-37 needs warp_size | threads_per_team), item = box
+      {"lavamd", 512, 128, 32, 1, HPAC_MAP_PER_TEAM},
   };
   if (!benchmark) return fail(err, el, HPAC_ERR_CONFIG, "benchmark is null");
   const Info* info = nullptr;
