@@ -1030,7 +1030,12 @@ ORACLE_API int oracle_kmeans_benchmark(const double* points, int64_t n, int dims
     hpac_stats_t st;
     if (spec && spec->technique == HPAC_TECH_PERFO && spec->perfo_kind == HPAC_PERFO_RANDOM)
       sp.perfo_seed = perfo_seed_base + (uint64_t)iter;
-    rc = oracle_run_region(g, n, HPAC_MAP_PER_THREAD, &r, spec ? &sp : NULL, &st, NULL, err, el);
+    /* RANDOM extension: the first iteration is exact (a skipped point must
+       have a stale label to keep; the reference modes keep label 0) */
+    const int exact_iter = spec && spec->technique == HPAC_TECH_PERFO &&
+                           spec->perfo_kind == HPAC_PERFO_RANDOM && iter == 1;
+    rc = oracle_run_region(g, n, HPAC_MAP_PER_THREAD, &r, (spec && !exact_iter) ? &sp : NULL, &st,
+                           NULL, err, el);
     if (rc) break;
     total->total_invocations += st.total_invocations;
     total->approx_invocations += st.approx_invocations;

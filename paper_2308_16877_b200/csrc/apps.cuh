@@ -121,17 +121,44 @@ struct AppBlackScholes : AppBase {
 // are the k distances; the host argmin (kmeans.hpp:111-121) is fused here,
 // so the engine payload is the label (stored as a double) and the k
 // distances are written only when the caller asks for them (region.out).
-// Centroids are staged once per CTA in shared memory (broadcast reads).
-// Default arithmetic is the reference's order without contraction, so
-// distances and labels are bit-identical to the CPU; the argmin takes a
-// sqrt only when a squared distance improves (sqrt is monotone, so the
-// strict-< / lowest-index result is unchanged).
+// Centroids (and their squared norms) are staged once per CTA in shared
+// memory (broadcast reads).
+//
+// Labels are bit-identical to the reference's (sqrt of the no-FMA,
+// dimension-order sum, strict <, lowest index) but are found with a filter:
+// d2(c) ~= |x|^2 + |c|^2 - 2 x.c costs one DFMA per (c, d) instead of three
+// FP64 ops; with a rigorous error bound E(c) (a multiple of the unit
+// roundoff times |x|^2 + |c|^2, covering both this estimate and the
+// reference's own rounding) the estimated minimiser is the reference's
+// argmin whenever every other centroid's estimate exceeds it by more than
+// E(best) + E(other) (+16 ulp so the sqrt values cannot collide). Any
+// closer pair (near-ties, duplicate centroids, non-finite data) re-runs the
+// reference computation over all centroids.
 struct AppKmeans : AppBase {
+#ifndef HPAC_KM_MINB
+#define HPAC_KM_MINB 2
+#endif
+  // the point (32 doubles) lives in registers: cap at 128 so >= 16 warps fit
+  static constexpr int MIN_BLOCKS_256 = HPAC_KM_MINB;
   static constexpr int IN_MAX = 32;
   static constexpr int OUT_MAX = 1;
   __device__ static void init(const EngineParams& p, double* scratch) {
-    const int kd = p.region.kmeans_k * p.region.kmeans_dims;
+    const int k = p.region.kmeans_k, dims = p.region.kmeans_dims;
+    const int kd = k * dims;
     for (int i = threadIdx.x; i < kd; i += blockDim.x) scratch[i] = p.region.centroids[i];
+    __syncthreads();
+    double* cc = scratch + kd;  // [k] squared norms, then [1] their maximum
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+      double s = 0.0;
+      for (int d = 0; d < dims; ++d) s = fma(scratch[c * dims + d], scratch[c * dims + d], s);
+      cc[c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int c = 0; c < k; ++c) m = fmax(m, cc[c]);  // NaN norms: caught by chk
+      cc[k] = m;
+    }
     __syncthreads();
   }
   __device__ static void load(const EngineParams& p, int64_t idx, double (&in)[IN_MAX]) {
@@ -151,11 +178,9 @@ struct AppKmeans : AppBase {
         if (d < dims) in[d] = __ldg(src + d);
     }
   }
-  __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&in)[IN_MAX],
-                              double (&out)[OUT_MAX], const double* cent, int, int) {
-    const int dims = p.region.kmeans_dims, k = p.region.kmeans_k;
-    const bool fast = (p.region.flags & HPAC_REGION_KMEANS_FAST_MATH) != 0;
-    double* dist = p.region.out ? p.region.out + idx * k : nullptr;
+  // reference distances: sqrt of the dimension-order sum without contraction
+  __device__ static int exact_argmin(const double (&in)[IN_MAX], const double* cent, int dims,
+                                     int k, bool fast, double* dist) {
     int best = 0;
     double best_ssq = 0.0, best_d = 0.0;
     for (int c = 0; c < k; ++c) {
@@ -182,12 +207,12 @@ struct AppKmeans : AppBase {
         if (c == 0 || dd < best_d) {
           best = c;
           best_d = dd;
-          best_ssq = ssq;
         }
       } else if (c == 0) {
         best_ssq = ssq;
         best_d = __dsqrt_rn(ssq);
       } else if (ssq < best_ssq) {
+        // sqrt is monotone: only an improving squared distance can win
         double dd = __dsqrt_rn(ssq);
         if (dd < best_d) {
           best = c;
@@ -196,6 +221,84 @@ struct AppKmeans : AppBase {
         }
       }
     }
+    return best;
+  }
+  // rare fallback, out of line so the fast path keeps its registers: the
+  // point is re-read from global memory
+  __device__ static __noinline__ int exact_argmin_reload(const EngineParams& p, int64_t idx,
+                                                         const double* cent) {
+    double x[IN_MAX];
+    load(p, idx, x);
+    return exact_argmin(x, cent, p.region.kmeans_dims, p.region.kmeans_k, false, nullptr);
+  }
+  __device__ static bool eval(const EngineParams& p, int64_t idx, const double (&in)[IN_MAX],
+                              double (&out)[OUT_MAX], const double* cent, int, int) {
+    const int dims = p.region.kmeans_dims, k = p.region.kmeans_k;
+    const bool fast = (p.region.flags & HPAC_REGION_KMEANS_FAST_MATH) != 0;
+    double* dist = p.region.out ? p.region.out + idx * k : nullptr;
+    if (dist || fast || dims != IN_MAX || (k & 3) || k < 2) {
+      out[0] = (double)exact_argmin(in, cent, dims, k, fast, dist);
+      return true;
+    }
+    const double* cc = cent + k * dims;
+    double xx0 = 0.0, xx1 = 0.0;
+#pragma unroll
+    for (int d = 0; d < IN_MAX; d += 2) {
+      xx0 = fma(in[d], in[d], xx0);
+      xx1 = fma(in[d + 1], in[d + 1], xx1);
+    }
+    const double xx = xx0 + xx1;
+    // E = G (|x|^2 + max_c |c|^2) bounds |estimate - reference ssq| for every
+    // centroid: 4x the (4d+8)u first-order bound
+    const double G = 4.0 * (4.0 * IN_MAX + 8.0) * 0x1.0p-53;
+    const double E = G * (xx + cc[k]);
+    int best = 0;
+    double m1 = dinf(), m2 = dinf(), chk = 0.0;
+    // four centroids per pass (eight independent DFMA chains per thread);
+    // the next dimension pair's centroid values are loaded one step ahead so
+    // the shared-memory latency overlaps the FMAs
+    for (int c = 0; c < k; c += 4) {
+      const double2* c0 = reinterpret_cast<const double2*>(cent + c * IN_MAX);
+      double acc[4][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+      double2 u[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[j] = c0[j * (IN_MAX / 2)];
+#pragma unroll
+      for (int d = 0; d < IN_MAX; d += 2) {
+        double2 v[4];
+        if (d + 2 < IN_MAX) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = c0[j * (IN_MAX / 2) + d / 2 + 1];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[j][0] = fma(in[d], u[j].x, acc[j][0]);
+          acc[j][1] = fma(in[d + 1], u[j].y, acc[j][1]);
+        }
+        if (d + 2 < IN_MAX) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) u[j] = v[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double a = fma(-2.0, acc[j][0] + acc[j][1], xx + cc[c + j]);
+        chk += a;  // NaN / inf anywhere -> reference path
+        if (a < m1) {
+          m2 = m1;
+          m1 = a;
+          best = c + j;
+        } else if (a < m2) {
+          m2 = a;
+        }
+      }
+    }
+    // every other centroid provably farther, by more than the bound on both
+    // estimates plus 16 ulp (so the reference's sqrt values cannot collide)
+    if (!(isfinite(chk) && m2 - m1 > 2.0 * E + 16.0 * 0x1.0p-53 * fabs(m2)))
+      best = exact_argmin_reload(p, idx, cent);
     out[0] = (double)best;
     return true;
   }

@@ -525,8 +525,8 @@ size_t engine_thread_smem(EngineParams& p) {
     off += (size_t)p.tsize * (p.in_dims + p.out_dims) * p.wpt * p.tpw;
   off = (off + 1) & ~(size_t)1;  // 16-byte aligned scratch (vector staging)
   p.smem_scratch_off = (int)off;
-  if (p.region.app == HPAC_APP_KMEANS)
-    off += (size_t)p.region.kmeans_k * p.region.kmeans_dims;
+  if (p.region.app == HPAC_APP_KMEANS)  // centroids + squared norms
+    off += (size_t)p.region.kmeans_k * p.region.kmeans_dims + p.region.kmeans_k + 1;
   if (p.region.app == HPAC_APP_LAVAMD) off += (size_t)p.region.lavamd_particles * 5;
   p.smem_ctl_off = (int)off;
   // control ints: 16 fixed + generic-ws words (4 per logical warp + 3 per table)

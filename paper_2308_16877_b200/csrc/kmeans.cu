@@ -189,7 +189,12 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     if (spec && spec->technique == HPAC_TECH_PERFO && spec->perfo_kind == HPAC_PERFO_RANDOM)
       sp.perfo_seed = pb->perfo_seed_base + (uint64_t)iter;
     hpac_stats_t s{};
-    rc = hpac_run_region(grid, n, HPAC_MAP_PER_THREAD, &r, spec ? &sp : nullptr, &L, &s, err, el);
+    // RANDOM extension: the first iteration is exact (a skipped point must
+    // have a stale label to keep; the reference modes keep label 0)
+    const bool exact_iter = spec && spec->technique == HPAC_TECH_PERFO &&
+                            spec->perfo_kind == HPAC_PERFO_RANDOM && iter == 1;
+    rc = hpac_run_region(grid, n, HPAC_MAP_PER_THREAD, &r, (spec && !exact_iter) ? &sp : nullptr,
+                         &L, &s, err, el);
     if (rc) {
       res->stats.arena_required = s.arena_required;
       res->stats.arena_available = s.arena_available;
