@@ -45,7 +45,16 @@ WORKLOADS = {
         name="lavamd-64^3-boxes-x-128-taf-warp", benchmark="lavamd", boxes1d=64, particles=128, ipt=1,
         directive="memo(out:3:8:0.1) level(warp)", spec=("taf", 3, 8, 0.1, "warp"),
         compare_levels=("thread", "team"), unit="particles/s"),
+    # C3 as the reference's kmeans_benchmark (bench/kmeans.hpp:62-144): the
+    # whole Lloyd loop (region + centroid update + per-iteration all-reduce),
+    # to convergence or 40 iterations; one step = one full run
     "kmeans": dict(
+        name="kmeans-lloyd-16M-x-32-x-64-perfo-random-warp", benchmark="kmeans_lloyd", n=1 << 24,
+        dims=32, k=64, ipt=4, separation=30.0, max_iters=40,
+        directive="perfo(random:50) level(warp)", spec=("perfo", "random", 50, "warp"),
+        unit="point-iterations/s"),
+    # one distance-region launch with a reference perforation kind
+    "kmeans-region": dict(
         name="kmeans-16M-x-32-x-64-perfo-small", benchmark="kmeans", n=1 << 24, dims=32, k=64,
         ipt=4, directive="perfo(small:2)", spec=("perfo", "small", 2), unit="point-iterations/s"),
 }
@@ -77,6 +86,12 @@ def binomial_flops(N):
 
 def kmeans_flops(d, k):
     return 3.0 * d * k + k  # sub, mul, add per (c, d) + sqrt per centroid
+
+
+def kmeans_filter_flops(d, k):
+    # executed filter (apps.cuh AppKmeans::eval): x.c as one DFMA per (c, d),
+    # |x|^2 (d DFMA), per centroid |x|^2+|c|^2, -2 dot, compare: 2dk + 2d + 3k
+    return 2.0 * d * k + 2.0 * d + 3.0 * k
 
 
 # LavaMD pair term (apps.cuh AppLavaMD::eval): dot 5, r2 2, exponent arg 1,
@@ -169,7 +184,7 @@ def make_spec(E, s):
         return E.iact(s[1], s[2], s[3], s[4])
     if s[0] == "taf":
         return E.taf(s[1], s[2], s[3], s[4])
-    return E.perfo(s[1], s[2])
+    return E.perfo(s[1], s[2], level=s[3] if len(s) > 3 else "thread")
 
 
 # ------------------------------------------------------------------ reference arm
@@ -186,7 +201,7 @@ def reference_arm(args, wl):
     if rank != 0:
         return
     kind = "reference"
-    if wl["benchmark"] != "lavamd":
+    if wl["benchmark"] not in ("lavamd", "kmeans_lloyd"):
         oracle.ref()
     cores = os.cpu_count() or 1
     n = wl.get("n")
@@ -240,6 +255,32 @@ def reference_arm(args, wl):
                                             make_spec(E, wl["spec"]))
             assert rc == 0, msg
             return per * P * scale
+    elif wl["benchmark"] == "kmeans_lloyd":
+        # random perforation is not in the reference: the oracle
+        # port's kmeans_benchmark (same Lloyd loop and decisions) per worker
+        import ctypes as C
+        from paper_2308_16877_b200 import abi
+        d, k = wl["dims"], wl["k"]
+        per, iters = 1 << 12, 5
+        pts = E.make_blobs(per * 4, d, k, 42, wl["separation"])
+        kind = "port"
+        sample_desc = f"{cores} threads x {per} points x {iters} Lloyd iterations (oracle port kmeans_benchmark)"
+
+        def work(worker, step):
+            lo = ((worker + step) % 4) * per
+            sub = np.ascontiguousarray(pts[lo:lo + per])
+            lab = np.zeros(per, np.int32)
+            cen = np.zeros((k, d))
+            it_c, conv_c = C.c_int32(), C.c_int32()
+            stc = abi.Stats()
+            err = C.create_string_buffer(256)
+            g = E.GridConfig(per // 256, 64, 32, 4)
+            sp = make_spec(E, wl["spec"])
+            rc = oracle.oracle().oracle_kmeans_benchmark(sub.ctypes.data, per, d, k, C.byref(g.c()), C.byref(sp),
+                                                         iters, 7, lab.ctypes.data, cen.ctypes.data,
+                                                         C.byref(it_c), C.byref(conv_c), C.byref(stc), err, 256)
+            assert rc == 0, err.value
+            return per * it_c.value
     else:
         d, k = wl["dims"], wl["k"]
         per = 1 << 12
@@ -599,6 +640,169 @@ def our_arm(args, wl):
         dist.destroy_process_group()
 
 
+def kmeans_lloyd_arm(args, wl):
+    """C3: the Lloyd loop (hpac_kmeans_run) exact vs perforated on the same
+    synthetic points; per-GPU shard of n points, centroid partials
+    all-reduced over NCCL every iteration when N > 1 (weak scaling)."""
+    import numpy as np
+    import torch
+
+    from paper_2308_16877_b200 import distributed as D
+    from paper_2308_16877_b200 import engine as E
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    n, d, k = wl["n"], wl["dims"], wl["k"]
+    pts = E.make_blobs(n, d, k, 42 + rank, wl["separation"])
+    d_pts = torch.from_numpy(pts).to(dev)
+    # Forgy init from rank 0's first k points, identical on every rank
+    cent0 = torch.from_numpy(E.make_blobs(n, d, k, 42, wl["separation"])[:k].copy() if rank else pts[:k].copy()).to(dev)
+    grid, _ = E.resolve_grid("kmeans", n, items_per_thread=wl["ipt"])
+    spec = make_spec(E, wl["spec"])
+    allreduce = D.kmeans_allreduce_hook() if dist is not None else None
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def one(sp, seed):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        flush.zero_()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        r = E.kmeans_run(grid, d_pts, k, sp, max_iters=wl["max_iters"], centroids=cent0.clone(),
+                         perfo_seed_base=seed, allreduce=allreduce, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return r, ev0.elapsed_time(ev1)
+
+    def timed(sp):
+        for i in range(args.warmup):
+            one(sp, 1000 + i)
+        res = [one(sp, 7) for _ in range(args.steps)]
+        return res
+
+    ex = timed(None)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ap = timed(spec)
+    time.sleep(0.15)
+    clk = clocks.stop()
+    r_e, r_a = ex[-1][0], ap[-1][0]
+    t_e = sum(t for _, t in ex)
+    t_a = sum(t for _, t in ap)
+    reg_a = sum(r.region_ms for r, _ in ap)
+    if dist is not None:
+        t = torch.tensor([t_e, t_a, reg_a], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e, t_a, reg_a = t.tolist()
+    it_e, it_a = r_e.iterations, r_a.iterations
+    value = ws * n * it_a * args.steps / (t_a * 1e-3)
+    exact_value = ws * n * it_e * args.steps / (t_e * 1e-3)
+    mcr = E.mcr(r_e.assignments, r_a.assignments)
+
+    # end to end: pinned host points -> device, Lloyd loop, labels -> host
+    e2e = None
+    if args.e2e_steps > 0:
+        h_pts = torch.from_numpy(pts).pin_memory()
+        h_lab = torch.empty(n, dtype=torch.int32).pin_memory()
+        buf = torch.empty_like(d_pts)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        its = 0
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.e2e_steps):
+            buf.copy_(h_pts, non_blocking=True)
+            r = E.kmeans_run(grid, buf, k, spec, max_iters=wl["max_iters"], centroids=cent0.clone(),
+                             perfo_seed_base=7, allreduce=allreduce, stream=stream)
+            h_lab.copy_(r.assignments, non_blocking=True)
+            its += r.iterations
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        e2e_t = ev0.elapsed_time(ev1)
+        if dist is not None:
+            t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = t.item()
+        e2e = {"value": ws * n * its / (e2e_t * 1e-3), "unit": wl["unit"],
+               "h2d_bytes_per_step": n * d * 8, "d2h_bytes_per_step": n * 4, "steps": args.e2e_steps}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    import ctypes as C
+    from paper_2308_16877_b200 import abi
+    fp = C.c_double()
+    abi.lib().hpac_probe_fp64_peak(C.byref(fp))
+    st = r_a.stats
+    evaluated = (st["total_invocations"] - st["approx_invocations"]) * args.steps
+    achieved = evaluated * kmeans_filter_flops(d, k) / (reg_a * 1e-3) / 1e12
+    roof = {"bound": "fp64", "kernel": "distance region (engine_thread_kernel<AppKmeans>)",
+            "achieved": achieved, "peak": fp.value, "unit": "TFLOP/s",
+            "frac": achieved / fp.value if fp.value else None,
+            "peak_source": "in-run DFMA probe (hpac_probe_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
+            "algorithmic": f"{kmeans_filter_flops(d, k):.0f} FP64 flops per evaluated point-iteration "
+                           "(filtered argmin; reference order only on near-ties)",
+            "region_share_of_step": reg_a / t_a,
+            "traffic": load_traffic(wl["name"])}
+    cpu = None
+    if args.cpu_baseline and ws == 1:
+        try:
+            import oracle
+            # random perforation is not in the reference (SPEC.md:345): the
+            # oracle port's kmeans_benchmark on a bounded sample
+            m, iters = 1 << 13, 8
+            sub = np.ascontiguousarray(pts[:m])
+            lab = np.zeros(m, np.int32)
+            cen = np.zeros((k, d))
+            it_c, conv_c = C.c_int32(), C.c_int32()
+            stc = abi.Stats()
+            err = C.create_string_buffer(256)
+            g2 = E.GridConfig(m // 256, 64, 32, 4)
+            t0 = time.perf_counter()
+            rc = oracle.oracle().oracle_kmeans_benchmark(sub.ctypes.data, m, d, k, C.byref(g2.c()), C.byref(spec),
+                                                         iters, 7, lab.ctypes.data, cen.ctypes.data,
+                                                         C.byref(it_c), C.byref(conv_c), C.byref(stc), err, 256)
+            dt = time.perf_counter() - t0
+            assert rc == 0, err.value
+            cpu = {"value": m * it_c.value / dt, "unit": wl["unit"], "cores": 1, "kind": "port",
+                   "sample": f"{m} points, kmeans_benchmark for {it_c.value} iterations (oracle port), 1 thread"}
+        except Exception as exc:
+            cpu = {"value": None, "unit": wl["unit"], "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": wl["unit"], "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_a / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic make_blobs(separation {wl['separation']}), seed 42 + rank",
+        "config": {"workload": wl["name"], "n_per_gpu": n, "dims": d, "k": k, "directive": wl["directive"],
+                   "max_iters": wl["max_iters"], "step": "one full Lloyd run (kmeans_benchmark)",
+                   "grid": {"num_teams": grid.num_teams, "threads_per_team": grid.threads_per_team,
+                            "warp_size": grid.warp_size, "items_per_thread": grid.items_per_thread},
+                   "l2": "flushed before every timed run; 4.3 GB of points per GPU >> L2",
+                   "parallelism": f"dp{ws} (points sharded, NCCL all-reduce of centroid partials per iteration)"},
+        "speedup_vs_exact": value / exact_value,
+        "time_to_solution_speedup": t_e / t_a,
+        "exact_value": exact_value,
+        "iterations": {"exact": it_e, "approx": it_a},
+        "converged": {"exact": r_e.converged, "approx": r_a.converged},
+        "quality": {"mcr": mcr}, "quality_ok": bool(mcr <= 0.01),
+        "approx_rate": st["approx_invocations"] / max(1, st["total_invocations"]),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": args.steps * (2 * it_a), "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -612,6 +816,8 @@ def main():
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, wl)
+    elif wl["benchmark"] == "kmeans_lloyd":
+        kmeans_lloyd_arm(args, wl)
     else:
         our_arm(args, wl)
 

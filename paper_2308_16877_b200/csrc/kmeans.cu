@@ -47,42 +47,97 @@ __global__ void kmeans_init_labels(int32_t* dist_label, int32_t* assign, int64_t
 }
 
 // Per-CTA partials: [k*dims sums | k counts | changed] into part[cta][...].
+// A warp walks its contiguous chunk 32 points at a time: lane j reads point
+// j's label and updates its assignment (coalesced), then the warp streams
+// the 32 rows (lane = dimension, 256 B per row) with kBatch row loads in
+// flight before accumulating them, in point order, into the warp's private
+// shared-memory sums. Counts are integers (exact in any order).
+constexpr int kBatch = 32;
 __global__ void __launch_bounds__(kUpdWarps * 32)
-    kmeans_update_partial(const double* pts, const int32_t* dist_label, int32_t* assign,
-                          int64_t n, int dims, int k, int64_t chunk, double* part) {
-  extern __shared__ __align__(16) double acc[];  // [warps][k*dims + k]
+    kmeans_update_partial(const double* __restrict__ pts, const int32_t* __restrict__ dist_label,
+                          int32_t* __restrict__ assign, int64_t n, int dims, int k, int64_t chunk,
+                          double* __restrict__ part) {
+  extern __shared__ __align__(16) double acc[];  // [warps][k*dims] then int counts [warps][k]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int kd = k * dims, stride = kd + k;
-  double* my = acc + (size_t)w * stride;
-  for (int i = lane; i < stride; i += 32) my[i] = 0.0;
+  const int kd = k * dims;
+  double* my = acc + (size_t)w * kd;
+  int* cnts = reinterpret_cast<int*>(acc + (size_t)kUpdWarps * kd) + w * k;
+  for (int i = lane; i < kd; i += 32) my[i] = 0.0;
+  for (int i = lane; i < k; i += 32) cnts[i] = 0;
   __syncwarp();
   const int64_t gw = (int64_t)blockIdx.x * kUpdWarps + w;
   const int64_t lo = gw * chunk, hi = lo + chunk < n ? lo + chunk : n;
   unsigned long long changed = 0;
-  for (int64_t i = lo; i < hi; ++i) {
-    const int c = dist_label[i];
-    const double* x = pts + i * dims;
-    double* row = my + (size_t)c * dims;
-    for (int d = lane; d < dims; d += 32) row[d] += __ldcs(x + d);
-    if (lane == 0) {
-      my[kd + c] += 1.0;
-      if (assign[i] != c) {
-        ++changed;
-        assign[i] = c;
+  if (dims <= 32) {
+    // software-pipelined: batch b+1's rows and labels are in flight while
+    // batch b is accumulated
+    const bool dl = lane < dims;
+    double xa[kBatch], xb[kBatch];
+    int la = 0, lb = 0;
+    auto fetch = [&](int64_t b0, double (&x)[kBatch], int& lab) {
+      const int cnt = (int)(hi - b0 < kBatch ? hi - b0 : kBatch);
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j)
+        x[j] = (j < cnt && dl) ? __ldcs(pts + (b0 + j) * dims + lane) : 0.0;
+      lab = lane < cnt ? dist_label[b0 + lane] : 0;
+    };
+    if (lo < hi) fetch(lo, xa, la);
+    for (int64_t b0 = lo; b0 < hi; b0 += kBatch) {
+      const int cnt = (int)(hi - b0 < kBatch ? hi - b0 : kBatch);
+      if (b0 + kBatch < hi) fetch(b0 + kBatch, xb, lb);
+      if (lane < cnt) {
+        if (assign[b0 + lane] != la) {
+          ++changed;
+          assign[b0 + lane] = la;
+        }
+        atomicAdd(&cnts[la], 1);
       }
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const int c = __shfl_sync(0xffffffffu, la, j);
+        if (j < cnt && dl) my[(size_t)c * dims + lane] += xa[j];
+      }
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) xa[j] = xb[j];
+      la = lb;
     }
-    __syncwarp();
+  } else {
+    for (int64_t base = lo; base < hi; base += 32) {
+      const int cnt = (int)(hi - base < 32 ? hi - base : 32);
+      int c_l = 0;
+      if (lane < cnt) {
+        c_l = dist_label[base + lane];
+        if (assign[base + lane] != c_l) {
+          ++changed;
+          assign[base + lane] = c_l;
+        }
+        atomicAdd(&cnts[c_l], 1);
+      }
+      for (int j = 0; j < cnt; ++j) {
+        const int c = __shfl_sync(0xffffffffu, c_l, j);
+        for (int d = lane; d < dims; d += 32) my[(size_t)c * dims + d] += __ldcs(pts + (base + j) * dims + d);
+      }
+      __syncwarp();
+    }
   }
   __syncthreads();
   // fixed-order sum over the CTA's warps
+  const int stride = kd + k;
   double* out = part + (size_t)blockIdx.x * (stride + 1);
-  for (int j = threadIdx.x; j < stride; j += blockDim.x) {
+  for (int j = threadIdx.x; j < kd; j += blockDim.x) {
     double s = 0.0;
-    for (int v = 0; v < kUpdWarps; ++v) s += acc[(size_t)v * stride + j];
+    for (int v = 0; v < kUpdWarps; ++v) s += acc[(size_t)v * kd + j];
     out[j] = s;
   }
+  const int* allc = reinterpret_cast<const int*>(acc + (size_t)kUpdWarps * kd);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    long long s = 0;
+    for (int v = 0; v < kUpdWarps; ++v) s += allc[v * k + j];
+    out[kd + j] = (double)s;
+  }
   __shared__ unsigned long long ch[kUpdWarps];
-  if (lane == 0) ch[w] = changed;
+  const unsigned long long wsum = __reduce_add_sync(0xffffffffu, (unsigned)changed);
+  if (lane == 0) ch[w] = wsum;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
@@ -134,7 +189,7 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
   if (n < 0 || dims < 1 || k < 1 || pb->max_iters < 0)
     return kfail(err, el, HPAC_ERR_CONFIG, "kmeans problem: bad sizes");
   const size_t stride = (size_t)k * dims + k;
-  const size_t upd_smem = (size_t)kUpdWarps * stride * sizeof(double);
+  const size_t upd_smem = (size_t)kUpdWarps * ((size_t)k * dims * sizeof(double) + (size_t)k * sizeof(int)) + 16;
   if (upd_smem > 200 * 1024)
     return kfail(err, el, HPAC_ERR_UNSUPPORTED, "k*dims too large for the centroid update (%zu B)",
                  upd_smem);

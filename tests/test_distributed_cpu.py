@@ -132,7 +132,7 @@ def test_bench_reference_arm_under_torchrun():
     """N=2: rank 0 alone runs the reference arm and prints; rank 1 exits 0."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29513", str(ROOT / "bench.py"),
-           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--workload", "kmeans"]
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--workload", "kmeans-region"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
