@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_ker
     tma_load_1d(tile, in + team_base * kRec, (uint32_t)(tpt * kRec * 8), &bar[0]);
   }
   bool loaded_cur = p.steps > 0 && tile_tma(0);
-  bool issued0 = loaded_cur, issued1 = false;  // thread 0's bookkeeping
+  // thread 0's bookkeeping: a load into buffer b that no consumer waited for
+  // is still "outstanding"; it must be retired before the buffer is re-armed
+  // (an mbarrier must not see a second arrive while its phase is pending)
+  bool issued0 = loaded_cur, issued1 = false;
 
   // TAF state (TafState, taf.hpp:59-163): register shift register, oldest first
   int taf_mode = kTafFilling, taf_rem = 0, taf_count = 0;
@@ -182,6 +185,7 @@ __global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_ker
       loaded_next = true;
       if (local == 0) {
         const int nb = buf ^ 1;
+        if (nb ? issued1 : issued0) mbar_wait(&bar[nb], (nb ? phase1 : phase0) ^ 1);
         mbar_expect_tx(&bar[nb], (uint32_t)(tpt * kRec * 8));
         tma_load_1d(tile + nb * tpt * kRec, in + (team_base + (step + 1) * G) * kRec,
                     (uint32_t)(tpt * kRec * 8), &bar[nb]);

@@ -40,6 +40,7 @@ SHAPES = [  # (num_teams, tpt, ws, ipt, n)
     (9, 128, 16, 4, 9 * 128 * 3 + 65),
     (5, 256, 32, 3, 5 * 256 * 3 - 300),
     (64, 64, 4, 16, 64 * 64 * 16),
+    (1024, 64, 32, 16, 1024 * 64 * 16),  # C1 shape at 1/4 size
 ]
 SPECS = [
     lambda: None,
@@ -52,6 +53,11 @@ SPECS = [
     lambda: E.perfo("fini", 30),
     lambda: E.perfo("random", 40, seed=9, level="team"),
     lambda: E.perfo("herded_large", 3),
+    # approximate steps where no lane waits on a prefetched tile (the buffer
+    # is re-armed two steps later: the engine must retire the old copy first)
+    lambda: E.taf(5, 2, 0.1, "warp"),
+    lambda: E.taf(5, 8, 0.5, "team"),
+    lambda: E.taf(2, 1, 1.0, "warp"),
 ]
 
 
