@@ -609,6 +609,27 @@ HPAC_API int hpac_stats_fetch(hpac_stats_t* stats) {
   return finish_status(g_scratch.h_cnt, stats, -1, buf, sizeof buf);
 }
 
+// Private stream-ordered pool for the host-buffer entry: memory is kept
+// across calls (release threshold = max), so repeated end-to-end calls do
+// not re-map device memory every time (the default pool trims at syncs).
+cudaMemPool_t host_entry_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) return pools[dev] = nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  return pools[dev];
+}
+
 // End-to-end entry with host buffers: H2D inputs, run, D2H outputs.
 HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
                                   const hpac_region_t* host_region, const hpac_spec_t* spec,
@@ -653,7 +674,10 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
   auto dalloc = [&](size_t bytes, const void* src, bool copy) -> void* {
     if (!bytes) return nullptr;
     void* d = nullptr;
-    if (cudaMallocAsync(&d, bytes, st) != cudaSuccess) return nullptr;
+    cudaMemPool_t pool = host_entry_pool();
+    if ((pool ? cudaMallocFromPoolAsync(&d, bytes, pool, st) : cudaMallocAsync(&d, bytes, st)) !=
+        cudaSuccess)
+      return nullptr;
     bufs.push_back(d);
     if (copy && src) cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
     return d;
