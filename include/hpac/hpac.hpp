@@ -239,6 +239,22 @@ inline Region kmeans_region(const double* points, int dims, const double* centro
   return g;
 }
 
+// LavaMD (extension): one home box per item under
+// WorkMapping::kPerTeam with threads_per_team == particles; rv (v,x,y,z) and
+// qv per particle (32-byte aligned rv), fv accumulated in place.
+inline Region lavamd_region(const double* rv, const double* qv, double* fv, int boxes1d, int particles,
+                            double alpha = 0.5) {
+  Region g;
+  g.r.app = HPAC_APP_LAVAMD;
+  g.r.in = rv;
+  g.r.table_out = qv;
+  g.r.out = fv;
+  g.r.lavamd_boxes1d = boxes1d;
+  g.r.lavamd_particles = particles;
+  g.r.lavamd_alpha = alpha;
+  return g;
+}
+
 // ---- launch (engine.hpp:35-54, :132-134) --------------------------------------
 struct KernelStats {
   uint64_t total_invocations = 0, approx_invocations = 0, divergent_warp_steps = 0,

@@ -311,6 +311,32 @@ static void kmeans_small() {  // test_bench.cpp:139-163
   CHECK(r.converged && r.iterations <= 2);
 }
 
+static void lavamd_levels() {  // extension: TAF at warp vs team, staging outside the region
+  const int b1 = 4, P = 64, nb = b1 * b1 * b1;
+  std::vector<double> rv(nb * P * 4), qv(nb * P);
+  hpac_make_lavamd(b1, P, 3, rv.data(), qv.data());
+  const std::vector<double> zero(nb * P * 4, 0.0);
+  Dev<double> drv(rv), dqv(qv), fe(zero), fw(zero), ft(zero);
+  GridConfig g = grid_of(nb, P, 32, 1);
+  auto e = run_region(g, nb, WorkMapping::kPerTeam, lavamd_region(drv.p, dqv.p, fe.p, b1, P), nullptr);
+  ApproxSpec w = parse_directive("memo(out:2:4:0.2) out(fv[i:4]) level(warp)");
+  ApproxSpec t = parse_directive("memo(out:2:4:0.2) out(fv[i:4]) level(team)");
+  auto rw = run_region(g, nb, WorkMapping::kPerTeam, lavamd_region(drv.p, dqv.p, fw.p, b1, P), &w);
+  auto rt = run_region(g, nb, WorkMapping::kPerTeam, lavamd_region(drv.p, dqv.p, ft.p, b1, P), &t);
+  CHECK(e.stats.approx_invocations == 0 && e.stats.total_invocations == rw.stats.total_invocations);
+  CHECK(rw.stats.divergent_warp_steps == 0 && rt.stats.divergent_warp_steps == 0);
+  CHECK(rw.stats.approx_invocations % 32 == 0 && rt.stats.approx_invocations % P == 0);
+  CHECK(rt.stats.approx_invocations > 0);
+  bool threw = false;
+  try {
+    run_region(grid_of(nb, 2 * P, 32, 1), nb, WorkMapping::kPerTeam, lavamd_region(drv.p, dqv.p, fe.p, b1, P),
+               nullptr);
+  } catch (const ConfigError&) {
+    threw = true;  // particles must equal threads_per_team
+  }
+  CHECK(threw);
+}
+
 int main() {
   std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"baseline_accurate", baseline_accurate}, {"taf_threshold_zero_noise", taf_threshold_zero_noise},
@@ -321,7 +347,7 @@ int main() {
       {"team_vote_multiples", team_vote_multiples}, {"tail_masking", tail_masking},
       {"per_team_mapping", per_team_mapping}, {"arena_overflow", arena_overflow},
       {"deterministic", deterministic}, {"directives_and_grid", directives_and_grid},
-      {"kmeans_small", kmeans_small}};
+      {"kmeans_small", kmeans_small}, {"lavamd_levels", lavamd_levels}};
   for (auto& [name, fn] : cases) {
     int before = g_fail;
     try {
