@@ -268,6 +268,16 @@ int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_t* proble
                     const hpac_spec_t* spec, void* stream, hpac_kmeans_result_t* result,
                     char* err, size_t errlen);
 
+/* Native NCCL all-reduce usable as hpac_kmeans_problem_t.allreduce:
+   `user` = the caller's ncclComm_t; sums the packed buffer in place on the
+   given stream. NCCL is loaded at run time (libnccl.so.2); 0 = unavailable. */
+int hpac_nccl_available(void);
+void hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream);
+/* ncclCommInitAll over `ndev` local devices (one process owning them all);
+   comms receives ndev ncclComm_t handles. */
+int hpac_nccl_comm_init_all(int ndev, const int* devlist, void** comms);
+int hpac_nccl_comm_destroy(void* comm);
+
 /* ---- host generators (same libstdc++ distributions as the reference) --- */
 int hpac_make_bs_portfolio(int64_t n, uint64_t seed, int32_t base_block, double jitter,
                            double* out /* n*5 */);

@@ -1,0 +1,71 @@
+// nccl_hook.cpp — native NCCL all-reduce for the K-Means Lloyd loop's
+// per-iteration centroid partials (hpac_kmeans_problem_t.allreduce), so a C++
+// driver shards points across the GPUs of a node without Python:
+//
+//   ncclComm_t comm;  ncclCommInitRank(&comm, nranks, id, rank);   // caller's
+//   pb.allreduce = hpac_nccl_allreduce;  pb.allreduce_user = comm;
+//   hpac_kmeans_run(&grid, &pb, spec, stream, &res, err, sizeof err);
+//
+// NCCL is resolved at run time (dlopen "libnccl.so.2"): the library keeps no
+// link-time NCCL dependency and shares whichever libnccl the process already
+// loaded (e.g. the one torch ships). ncclAllReduce(sum, double) in place on
+// the caller's stream, over NVLink/NVSwitch within a node.
+#include <dlfcn.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+
+#include "hpac_offload.h"
+
+#define HPAC_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+typedef int (*AllReduceFn)(const void*, void*, size_t, int /*dtype*/, int /*op*/, void* /*comm*/,
+                           void* /*stream*/);
+typedef int (*InitAllFn)(void** /*comms*/, int, const int*);
+typedef int (*DestroyFn)(void*);
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h ncclDataType_t / ncclRedOp_t
+
+struct Nccl {
+  void* h = nullptr;
+  AllReduceFn all_reduce = nullptr;
+  InitAllFn init_all = nullptr;
+  DestroyFn destroy = nullptr;
+};
+
+Nccl* nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!n.h) return;
+    n.all_reduce = reinterpret_cast<AllReduceFn>(dlsym(n.h, "ncclAllReduce"));
+    n.init_all = reinterpret_cast<InitAllFn>(dlsym(n.h, "ncclCommInitAll"));
+    n.destroy = reinterpret_cast<DestroyFn>(dlsym(n.h, "ncclCommDestroy"));
+  });
+  return n.all_reduce ? &n : nullptr;
+}
+}  // namespace
+
+HPAC_API int hpac_nccl_available(void) { return nccl() != nullptr; }
+
+// hpac_allreduce_fn: `user` is the caller's ncclComm_t
+HPAC_API void hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream) {
+  Nccl* n = nccl();
+  if (n && user) n->all_reduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, user, stream);
+}
+
+// Single-process communicators over `ndev` local devices (ncclCommInitAll),
+// for drivers and tests that own every GPU of the node in one process.
+HPAC_API int hpac_nccl_comm_init_all(int ndev, const int* devlist, void** comms) {
+  Nccl* n = nccl();
+  if (!n || !n->init_all) return HPAC_ERR_UNSUPPORTED;
+  return n->init_all(comms, ndev, devlist) == 0 ? HPAC_OK : HPAC_ERR_CUDA;
+}
+
+HPAC_API int hpac_nccl_comm_destroy(void* comm) {
+  Nccl* n = nccl();
+  if (!n || !n->destroy) return HPAC_ERR_UNSUPPORTED;
+  return n->destroy(comm) == 0 ? HPAC_OK : HPAC_ERR_CUDA;
+}

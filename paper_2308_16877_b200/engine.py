@@ -358,10 +358,13 @@ class KmeansResult:
 
 
 def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=None,
-               fast_math=False, perfo_seed_base=0, allreduce=None, stream=None) -> KmeansResult:
+               fast_math=False, perfo_seed_base=0, allreduce=None, stream=None,
+               nccl_comm=None) -> KmeansResult:
     """kmeans_benchmark (bench/kmeans.hpp:62-144) on the device. `points` is a
     torch CUDA tensor n x d. `allreduce(buf_tensor)` (optional) all-reduces the
-    packed [sums | counts | changed] partials across ranks each iteration."""
+    packed [sums | counts | changed] partials across ranks each iteration;
+    `nccl_comm` (an ncclComm_t handle) uses the library's native NCCL hook
+    (hpac_nccl_allreduce) instead."""
     import torch
     n, d = points.shape
     cent = torch.empty((k, d), dtype=torch.float64, device=points.device) if centroids is None else centroids
@@ -376,7 +379,10 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
     pb.perfo_seed_base = perfo_seed_base
     pb.reduce_buf = _ptr(red)
     cb = None
-    if allreduce is not None:
+    if nccl_comm is not None:
+        pb.allreduce = C.cast(abi.lib().hpac_nccl_allreduce, abi.ALLREDUCE_FN)
+        pb.allreduce_user = nccl_comm
+    elif allreduce is not None:
         def _cb(buf, count, user, st):
             allreduce(red)
         cb = abi.ALLREDUCE_FN(_cb)
@@ -391,6 +397,16 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
         _raise(rc, err, res.stats)
     return KmeansResult(assign, cent, res.iterations, bool(res.converged), res.stats.as_dict(),
                         res.region_ms, res.update_ms)
+
+
+def nccl_comms(ndev=1):
+    """Single-process NCCL communicators over devices 0..ndev-1 (ncclCommInitAll)."""
+    comms = (C.c_void_p * ndev)()
+    devs = (C.c_int * ndev)(*range(ndev))
+    rc = abi.lib().hpac_nccl_comm_init_all(ndev, devs, comms)
+    if rc:
+        raise UnsupportedError("NCCL unavailable") if rc == abi.ERR_UNSUPPORTED else CudaError("ncclCommInitAll")
+    return list(comms)
 
 
 # ---- generators (host) -----------------------------------------------------

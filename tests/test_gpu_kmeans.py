@@ -1,5 +1,7 @@
 """K-Means Lloyd loop on the device vs the oracle's kmeans_benchmark
 (bench/kmeans.hpp:62-144) and the reference's own kmeans tests."""
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
@@ -92,3 +94,22 @@ def test_allreduce_hook_two_identical_shards():
     assert len(calls) == twice.iterations == single.iterations
     assert torch.equal(single.assignments, twice.assignments)
     assert torch.allclose(single.centroids, twice.centroids, rtol=0, atol=0)
+
+
+def test_native_nccl_allreduce_hook():
+    """hpac_nccl_allreduce as the Lloyd loop's all-reduce hook (single-rank
+    NCCL communicator: the sum over one rank is the identity, so the run must
+    equal the hook-less one bit for bit)."""
+    if not abi.lib().hpac_nccl_available():
+        pytest.skip("libnccl.so.2 not loadable")
+    pts = E.make_blobs(8192, 8, 16, 9, 30.0)
+    grid, _ = E.resolve_grid("kmeans", 8192)
+    comm = E.nccl_comms(1)[0]
+    try:
+        a = E.kmeans_run(grid, dev(pts), 16, E.perfo("random", 25, seed=3), max_iters=20, perfo_seed_base=5)
+        b = E.kmeans_run(grid, dev(pts), 16, E.perfo("random", 25, seed=3), max_iters=20, perfo_seed_base=5,
+                         nccl_comm=comm)
+    finally:
+        abi.lib().hpac_nccl_comm_destroy(C.c_void_p(comm))
+    assert a.iterations == b.iterations
+    assert torch.equal(a.assignments, b.assignments) and torch.equal(a.centroids, b.centroids)
