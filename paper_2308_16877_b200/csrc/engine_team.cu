@@ -372,7 +372,11 @@ __device__ __forceinline__ void bt_phase(double (&v)[BMAX], int& L, int lo, int 
   double x0_last = x0;
   int L_last = L;
   for (int done = 0; L >= 0 && done < pmax; ++done) {
+    // the block range's top node may be the zero node jk+1 (live range
+    // capped at the highest in-the-money leaf): its right neighbour is 0,
+    // not lane 31's own v[0] that shfl_down returns
     double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+    if (lane == 31) vr = 0.0;
     double xa = x0, xb = fma(x0, q.up2, q.c2);
     const double xfirst = x0;
 #pragma unroll
@@ -447,26 +451,44 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
   // generous margin (the phase checks it anyway).
   int lo = (int)floor(((double)(N - 1 - kPhase) + log(strike / spot) / q.lnu) * 0.5) - 48;
   lo = max(0, min(lo, N / 2));
+  int jk = -1;  // highest in-the-money leaf
   for (int j = lo + lane; j <= N; j += 32) {
     double s = spot * exp((double)(2 * j - N) * q.lnu);
     double x = strike - s;
     xch[j] = x < 0.0 ? 0.0 : x;
+    if (x > 0.0) jk = j;
   }
+  jk = __reduce_max_sync(0xffffffffu, jk);
   __syncwarp();
+  // Zero region: node (j, L) only reaches leaves j..j+N-L, all out of the
+  // money when j > jk, and its exercise value is negative there too, so it
+  // is exactly +0 at every level (0*p + 0*q = +0). The live range is capped
+  // at jk (+ the zero right neighbour jk+1): the upper quarter of the
+  // triangle is never computed, and every computed node is unchanged.
+  const int top = jk + 1;
+  if (jk < lo) {
+    // no in-the-money leaf at or above the bound: with lo == 0 every node is
+    // exactly 0; otherwise let the full lattice handle it
+    if (jk < 0 && lo == 0) {
+      price = 0.0;
+      __syncwarp();
+      return true;
+    }
+    return false;
+  }
   int L = N - 1;
   while (L >= 0) {
-    const int live = L + 2 - lo;
-    if (live > 32 * kBtMax) return false;
+    const int live = min(L, jk) + 2 - lo;
+    if (live > 32 * kBtMax || live < 1) return false;
     {
-      const int lv = min(L + 1, kPhase);  // levels L .. L-lv+1 over nodes lo..level
-      nodes += (unsigned long long)lv * (unsigned long long)(L + 1 - lo) -
-               (unsigned long long)lv * (lv - 1) / 2;
+      const int lv = min(L + 1, kPhase);  // levels L .. L-lv+1 over nodes lo..min(level, jk)
+      for (int t = 0; t < lv; ++t) nodes += (unsigned long long)(min(L - t, jk) + 1 - lo);
     }
     bool ok = true;
     int nex = 0;
     const bool check = lo > 0;
 #define HPAC_BT(b, bn) \
-  if (live > 32 * (bn)) { bt_phase<b, BMAX>(v, L, lo, kPhase, q, lane, xch, check, ok, nex, N + 1); } else
+  if (live > 32 * (bn)) { bt_phase<b, BMAX>(v, L, lo, kPhase, q, lane, xch, check, ok, nex, top); } else
     HPAC_BT(20, 17) HPAC_BT(17, 14) HPAC_BT(14, 12) HPAC_BT(12, 10) HPAC_BT(10, 8) HPAC_BT(8, 7)
     HPAC_BT(7, 6) HPAC_BT(6, 5) HPAC_BT(5, 4) HPAC_BT(4, 3) HPAC_BT(3, 2) HPAC_BT(2, 1)
     HPAC_BT(1, 0) {}

@@ -275,3 +275,24 @@ def test_synthetic_bit_exact(profile, spec_fn):
     rc, st, msg = oracle.oracle_run(grid, n, mapping, E.synthetic_region(profile, 99, o_out), spec_fn(), o_paths)
     assert rc == 0, msg
     _compare(lr, st, out.cpu().numpy(), o_out, paths.cpu().numpy(), o_paths)
+
+
+@pytest.mark.parametrize("steps", [16, 40, 64, 96, 128, 200, 256, 512, 1000])
+def test_binomial_american_put_grid_of_moneyness(steps):
+    """The American-put lattice skips the exercise region below a tracked
+    bound and the exactly-zero region above the highest in-the-money leaf;
+    sweep moneyness / volatility / maturity so both edges land everywhere in
+    the lane blocks (incl. the block's top node being the zero node)."""
+    rng = np.random.default_rng(steps)
+    m = 192
+    S = 100.0 * np.ones(m)
+    K = S * np.exp(rng.uniform(np.log(0.6), np.log(1.6), m))
+    r = rng.uniform(0.0, 0.08, m)
+    vol = rng.uniform(0.05, 0.8, m)
+    T = rng.uniform(0.1, 3.0, m)
+    opts = np.stack([S, K, r, vol, T], 1)
+    want = oracle.binomial_prices(opts, steps)
+    out = torch.zeros(m, dtype=torch.float64, device="cuda")
+    lr = E.run_region(E.GridConfig(m, 64, 32, 1), m, 1, E.binomial_region(dev(opts), steps, out), None)
+    ok, worst = _rel_ok(out.cpu().numpy(), want)
+    assert ok, worst
