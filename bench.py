@@ -49,9 +49,9 @@ WORKLOADS = {
     # whole Lloyd loop (region + centroid update + per-iteration all-reduce),
     # to convergence or 40 iterations; one step = one full run
     "kmeans": dict(
-        name="kmeans-lloyd-16M-x-32-x-64-perfo-random-warp", benchmark="kmeans_lloyd", n=1 << 24,
+        name="kmeans-lloyd-16M-x-32-x-64-perfo-random-team", benchmark="kmeans_lloyd", n=1 << 24,
         dims=32, k=64, ipt=4, separation=30.0, max_iters=40,
-        directive="perfo(random:50) level(warp)", spec=("perfo", "random", 50, "warp"),
+        directive="perfo(random:52) level(team)", spec=("perfo", "random", 52, "team"),
         unit="point-iterations/s"),
     # one distance-region launch with a reference perforation kind
     "kmeans-region": dict(

@@ -58,6 +58,8 @@ def points(apps, quick=False):
             for p in (10, 25, 50):
                 for lv in ("thread", "warp"):
                     out.append(("kmeans", wl, f"perfo(random:{p}) {S['kmeans']} level({lv})"))
+            for p in (50, 52, 54, 56):  # team votes: the skip rate is a steep function of p
+                out.append(("kmeans", wl, f"perfo(random:{p}) {S['kmeans']} level(team)"))
             for kind, arg in (("small", 2), ("small", 4), ("large", 2)):
                 out.append(("kmeans", wl, f"perfo({kind}:{arg}) {S['kmeans']}"))
     if "lavamd" in apps:
