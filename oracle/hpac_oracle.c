@@ -388,25 +388,20 @@ typedef struct {
 
 /* LavaMD (extension; the framework's restatement of Rodinia lavaMD, SURVEY
    Appendix C; Rodinia is not under /root/reference, so parity is unpinned):
-   exp as Cody-Waite reduction + degree-12 Taylor in fma() Horner form, the
-   same sequence as the device code (fma() is exactly rounded on both). */
+   exp as a one-FMA reduction + a degree-11 polynomial in fma() Horner form,
+   the same sequence as the device code (fma() is exactly rounded on both). */
 static double lava_exp(double x) {
-  const double kd = rint(x * 1.4426950408889634);
-  double r = fma(-kd, 0x1.62e42fee00000p-1, x);
-  r = fma(-kd, 0x1.a39ef35793c76p-33, r);
-  double s = 1.0 / 479001600.0;
-  s = fma(s, r, 1.0 / 39916800.0);
-  s = fma(s, r, 1.0 / 3628800.0);
-  s = fma(s, r, 1.0 / 362880.0);
-  s = fma(s, r, 1.0 / 40320.0);
-  s = fma(s, r, 1.0 / 5040.0);
-  s = fma(s, r, 1.0 / 720.0);
-  s = fma(s, r, 1.0 / 120.0);
-  s = fma(s, r, 1.0 / 24.0);
-  s = fma(s, r, 1.0 / 6.0);
-  s = fma(s, r, 0.5);
-  s = fma(s, r, 1.0);
-  s = fma(s, r, 1.0);
+  static const double c[16] = {
+    1.4426950408889634, 0x1.62e42fefa39efp-1, 0x1.af8b4d5192f39p-26,
+    0x1.28ac933b441b4p-22, 0x1.71ddd52442153p-19, 0x1.a0199bbdcc2b9p-16,
+    0x1.a01a01c18b821p-13, 0x1.6c16c18319b74p-10, 0x1.111111110bf92p-7,
+    0x1.5555555551097p-5, 0x1.5555555555569p-3, 0x1.0000000000008p-1,
+    0x1.0000000000000p+0, 1.0, 0.0,
+    0x1.8p52};
+  const double kd = fma(x, c[0], c[15]) - c[15]; /* rint(x log2e), fused product */
+  const double r = fma(-kd, c[1], x);
+  double s = c[2];
+  for (int i = 3; i <= 13; ++i) s = fma(s, r, c[i]);
   return ldexp(s, (int)kd);
 }
 
@@ -462,10 +457,11 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
         const double* o2 = r->in + (b * P + j) * 4;
         const double q = r->table_out[b * P + j];
         /* Rodinia lavaMD pair term: r2 = rA.v + rB.v - dot(rA, rB),
-           vij = exp(-a2 r2), f += qB (vij, 2 vij (rA - rB)); FMA form */
-        const double dot = fma(me[3], o2[3], fma(me[2], o2[2], me[1] * o2[1]));
-        const double r2 = (me[0] + o2[0]) - dot;
-        const double vij = lava_exp(na2 * r2);
+           vij = exp(-a2 r2), f += qB (vij, 2 vij (rA - rB)); FMA form with
+           -a2 folded into rA (and into rB.v): x = (-a2 vA + -a2 vB) - dot(-a2 rA, rB) */
+        const double an = na2 * me[0], axn = na2 * me[1], ayn = na2 * me[2], azn = na2 * me[3];
+        const double dotn = fma(azn, o2[3], fma(ayn, o2[2], axn * o2[1]));
+        const double vij = lava_exp((an + na2 * o2[0]) - dotn);
         const double qv = q * vij;
         const double t = qv + qv;
         fv = fv + qv;

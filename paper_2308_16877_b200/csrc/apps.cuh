@@ -324,33 +324,41 @@ struct AppKmeans : AppBase {
 // Coefficients live in constant memory on the device so the DFMAs take them
 // as c[bank][offset] operands (64-bit immediates would otherwise be
 // re-materialised with two integer moves per use inside the pair loop).
+// [0] log2(e), [1] ln2 (rounded: one-FMA reduction, |k| small), [2..12] the
+// degree-11 polynomial a11..a1 (least-squares fit of e^r on |r| <= ln2/2 with
+// a0 = a1 = 1; tools/fit_exp.py), [13] a0, [15] the 1.5*2^52 shifter
 static __constant__ double kLavaExpC[16] = {
-    1.4426950408889634, 0x1.62e42fee00000p-1, 0x1.a39ef35793c76p-33,
-    1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
-    1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0, 0x1.8p52};
+    1.4426950408889634, 0x1.62e42fefa39efp-1, 0x1.af8b4d5192f39p-26,
+    0x1.28ac933b441b4p-22, 0x1.71ddd52442153p-19, 0x1.a0199bbdcc2b9p-16,
+    0x1.a01a01c18b821p-13, 0x1.6c16c18319b74p-10, 0x1.111111110bf92p-7,
+    0x1.5555555551097p-5, 0x1.5555555555569p-3, 0x1.0000000000008p-1,
+    0x1.0000000000000p+0, 1.0, 0.0,
+    0x1.8p52};
 
 __host__ __device__ __forceinline__ double lava_exp(double x) {
 #ifdef __CUDA_ARCH__
   const double* c = kLavaExpC;
-  // rint(x*log2e) via the 1.5*2^52 shifter (round-to-nearest-even, |t| < 2^51)
-  const double kd = __dsub_rn(__dadd_rn(__dmul_rn(x, c[0]), c[15]), c[15]);
+  // rint(x*log2e) via the 1.5*2^52 shifter on the fused product
+  const double kd = __dsub_rn(fma(x, c[0], c[15]), c[15]);
 #else
   static const double c[16] = {
-      1.4426950408889634, 0x1.62e42fee00000p-1, 0x1.a39ef35793c76p-33,
-      1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
-      1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0, 0x1.8p52};
-  const double kd = rint(x * c[0]);
+    1.4426950408889634, 0x1.62e42fefa39efp-1, 0x1.af8b4d5192f39p-26,
+    0x1.28ac933b441b4p-22, 0x1.71ddd52442153p-19, 0x1.a0199bbdcc2b9p-16,
+    0x1.a01a01c18b821p-13, 0x1.6c16c18319b74p-10, 0x1.111111110bf92p-7,
+    0x1.5555555551097p-5, 0x1.5555555555569p-3, 0x1.0000000000008p-1,
+    0x1.0000000000000p+0, 1.0, 0.0,
+    0x1.8p52};
+  const double kd = fma(x, c[0], c[15]) - c[15];
 #endif
-  double r = fma(-kd, c[1], x);
-  r = fma(-kd, c[2], r);
-  double s = c[3];  // 1/12!
+  const double r = fma(-kd, c[1], x);
+  double s = c[2];  // a11
 #pragma unroll
-  for (int i = 4; i <= 14; ++i) s = fma(s, r, c[i]);
-  s = fma(s, r, 1.0);
+  for (int i = 3; i <= 13; ++i) s = fma(s, r, c[i]);
   const int k = (int)kd;
 #ifdef __CUDA_ARCH__
-  // exact power-of-two scaling == ldexp while 2^k is a normal double
-  if (k > -1023 && k < 1024) return s * __longlong_as_double((long long)(k + 1023) << 52);
+  // exact power-of-two scaling == ldexp while the result stays normal: add
+  // k to the exponent field (s in [0.7, 1.42]) on the integer pipe
+  if (k > -1021 && k < 1022) return __longlong_as_double(__double_as_longlong(s) + ((long long)k << 52));
 #endif
   return ldexp(s, k);
 }
@@ -396,6 +404,10 @@ __host__ __device__ __forceinline__ int64_t lava_neighbour_at(int64_t box, int b
 static __device__ __noinline__ double4 lava_box_contribution(const double* rv_home, const double* s, int P,
                                                       double na2) {
   const double4 me = *reinterpret_cast<const double4*>(rv_home);
+  // exponent argument -a2 (vA + vB - dot) with -a2 folded into the home
+  // particle (once) and into the staged vB (staging): 5 ops instead of 6
+  const double an = __dmul_rn(na2, me.x), axn = __dmul_rn(na2, me.y), ayn = __dmul_rn(na2, me.z),
+               azn = __dmul_rn(na2, me.w);
   double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
 #ifndef HPAC_LAVA_UNROLL
 #define HPAC_LAVA_UNROLL 1  // measured: 1 (32.7 ms) < 4 (35.5) < 2 (36.5) at 32^3
@@ -405,18 +417,19 @@ static __device__ __noinline__ double4 lava_box_contribution(const double* rv_ho
   for (int j = 0; j < P; ++j) {
     const double2 b01 = *reinterpret_cast<const double2*>(s + j * 4);
     const double2 b23 = *reinterpret_cast<const double2*>(s + j * 4 + 2);
-    const double q = s[P * 4 + j];
-    const double dot = fma(me.w, b23.y, fma(me.z, b23.x, __dmul_rn(me.y, b01.y)));
-    const double r2 = __dsub_rn(__dadd_rn(me.x, b01.x), dot);
-    const double vij = lava_exp(__dmul_rn(na2, r2));
-    const double qv = __dmul_rn(q, vij);
-    const double t = __dadd_rn(qv, qv);
-    fv = __dadd_rn(fv, qv);
+    const double q2 = s[P * 4 + j];  // 2*qv, staged (exact doubling)
+    const double dotn = fma(azn, b23.y, fma(ayn, b23.x, __dmul_rn(axn, b01.y)));
+    const double vij = lava_exp(__dsub_rn(__dadd_rn(an, b01.x), dotn));  // b01.x = -a2 vB
+    // t = 2 q vij exactly as before (power-of-two scaling is exact); the
+    // potential is accumulated doubled and halved once at the end: the
+    // same bits as summing q*vij
+    const double t = __dmul_rn(q2, vij);
+    fv = __dadd_rn(fv, t);
     fx = fma(t, __dsub_rn(me.y, b01.y), fx);
     fy = fma(t, __dsub_rn(me.z, b23.x), fy);
     fz = fma(t, __dsub_rn(me.w, b23.y), fz);
   }
-  return make_double4(fv, fx, fy, fz);
+  return make_double4(0.5 * fv, fx, fy, fz);
 }
 
 struct AppLavaMD : AppBase {
@@ -444,8 +457,14 @@ struct AppLavaMD : AppBase {
         const int P = p.region.lavamd_particles;
         const double2* src = reinterpret_cast<const double2*>(p.region.in + b * P * 4);
         double2* dst = reinterpret_cast<double2*>(s);
-        for (int i = threadIdx.x; i < P * 2; i += blockDim.x) dst[i] = __ldg(src + i);
-        for (int i = threadIdx.x; i < P; i += blockDim.x) s[P * 4 + i] = __ldg(p.region.table_out + b * P + i);
+        const double na2 = -__dmul_rn(__dmul_rn(2.0, p.region.lavamd_alpha), p.region.lavamd_alpha);
+        for (int i = threadIdx.x; i < P * 2; i += blockDim.x) {
+          double2 v = __ldg(src + i);
+          if ((i & 1) == 0) v.x = __dmul_rn(na2, v.x);  // (v, x) half: stage -a2 v
+          dst[i] = v;
+        }
+        for (int i = threadIdx.x; i < P; i += blockDim.x)
+          s[P * 4 + i] = 2.0 * __ldg(p.region.table_out + b * P + i);
       }
     }
     __syncthreads();
