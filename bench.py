@@ -4,7 +4,9 @@
 
 Default workload (configs[1]): Binomial options, 1,048,576 American puts x
 1024-step CRR lattice under team-shared iACT input memoization
-(memo(in:...) level(team), kPerTeam mapping, 64-thread teams). One step =
+(memo(in:4:0.4) level(team), kPerTeam mapping, 64-thread teams, 384 items
+per team — the paper's items-per-thread knob: more options per team table,
+more reuse). One step =
 one pass of the region over the whole portfolio with inputs resident in
 HBM. Per-GPU work is fixed (weak scaling): each rank prices its own
 1,048,576-option shard; no collective on the data path.
@@ -35,8 +37,8 @@ METRIC = "approx-region items/s & speedup vs exact GPU kernel at <=1% quality lo
 WORKLOADS = {
     "binomial": dict(
         name="binomial-1M-x-1024-iact-team",
-        benchmark="binomial", n=1 << 20, lattice=1024, ipt=128,
-        directive="memo(in:4:0.5) level(team)", spec=("iact", 4, 0.5, None, "team"),
+        benchmark="binomial", n=1 << 20, lattice=1024, ipt=384,
+        directive="memo(in:4:0.4) level(team)", spec=("iact", 4, 0.4, None, "team"),
         unit="options/s"),
     "blackscholes": dict(
         name="blackscholes-4M-taf-h5", benchmark="blackscholes", n=1 << 22, ipt=16,

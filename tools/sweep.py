@@ -45,10 +45,10 @@ def points(apps, quick=False):
         for kind, arg in (("small", 2), ("small", 4), ("large", 2), ("random", 10), ("random", 25)):
             out.append(("blackscholes", wl, f"perfo({kind}:{arg}) {S['blackscholes']}"))
     if "binomial" in apps:
-        for ipt in ((128,) if quick else (64, 128)):
+        for ipt in ((128,) if quick else (64, 128, 384)):
             wl = dict(n=1 << 18, ipt=ipt)
             for ts in (2, 4, 8):
-                for thr in ((0.5,) if quick else (0.25, 0.5, 1.0)):
+                for thr in ((0.5,) if quick else (0.25, 0.4, 0.5, 1.0)):
                     out.append(("binomial", wl, f"memo(in:{ts}:{thr}) {S['binomial']} level(team)"))
             for kind, arg in (("small", 4), ("random", 25)):
                 out.append(("binomial", wl, f"perfo({kind}:{arg}) {S['binomial']} level(team)"))
