@@ -161,6 +161,31 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def gpu_index(local):
+    """LOCAL_RANK -> device. BENCH_DIST_BACKEND=gloo (multi-rank logic check on
+    a box with fewer GPUs than ranks) wraps ranks onto the available GPUs."""
+    import torch
+    if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "gloo":
+        return local % max(1, torch.cuda.device_count())
+    return local
+
+
+def init_dist(ws, local):
+    """One process per GPU: NCCL process group (barriers, max-over-ranks
+    timing, the K-Means all-reduce); BENCH_DIST_BACKEND=gloo for the
+    single-GPU check of the N>1 code path."""
+    if ws <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
+
+
 def load_traffic(workload):
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
@@ -393,11 +418,9 @@ def our_arm(args, wl):
     from paper_2308_16877_b200 import engine as E
 
     ws, rank, local = dist_env()
+    local = gpu_index(local)
     torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(ws, local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     n = wl.get("n")
@@ -663,11 +686,9 @@ def kmeans_lloyd_arm(args, wl):
     from paper_2308_16877_b200 import engine as E
 
     ws, rank, local = dist_env()
+    local = gpu_index(local)
     torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(ws, local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     n, d, k = wl["n"], wl["dims"], wl["k"]
