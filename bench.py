@@ -837,7 +837,9 @@ def kmeans_lloyd_arm(args, wl):
         "quality": {"mcr": mcr}, "quality_ok": bool(mcr <= 0.01),
         "approx_rate": st["approx_invocations"] / max(1, st["total_invocations"]),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": args.steps * (2 * it_a), "clocks": clk,
+        # per iteration: region, update partials, partial reduction, centroid
+        # recompute (not after the converged one); + the label init per run
+        "gpu_launches": args.steps * (4 * it_a + 1 - (1 if r_a.converged else 0)), "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
