@@ -37,6 +37,8 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
 // engine.hpp:29; 1 by default) and a per-round staging step executed by
 // every thread of the team outside the approximated region.
 struct AppBase {
+  // techniques the runtime accepts for the app (others are not instantiated)
+  static constexpr bool HAS_TAF = true, HAS_IACT = true;
   // occupancy hint for the 256-thread engine instantiation (launch bounds)
   static constexpr int MIN_BLOCKS_256 = 1;
   __device__ static int encounters(const EngineParams& p, int64_t idx) {
@@ -140,6 +142,7 @@ struct AppKmeans : AppBase {
 #endif
   // the point (32 doubles) lives in registers: cap at 128 so >= 16 warps fit
   static constexpr int MIN_BLOCKS_256 = HPAC_KM_MINB;
+  static constexpr bool HAS_TAF = false;  // rejected by the runtime (64-dim window)
   static constexpr int IN_MAX = 32;
   static constexpr int OUT_MAX = 1;
   __device__ static void init(const EngineParams& p, double* scratch) {
@@ -438,6 +441,7 @@ struct AppLavaMD : AppBase {
 #define HPAC_LAVA_MINB 3
 #endif
   static constexpr int MIN_BLOCKS_256 = HPAC_LAVA_MINB;
+  static constexpr bool HAS_IACT = false;  // no region inputs (iACT needs in(...))
   static constexpr int IN_MAX = 1;
   static constexpr int OUT_MAX = 4;
   __device__ static void init(const EngineParams&, double*) {}

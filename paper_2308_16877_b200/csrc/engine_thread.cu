@@ -503,9 +503,14 @@ static cudaError_t launch_tech(const EngineParams& p, int nblocks, size_t smem,
 
 template <class App>
 static cudaError_t launch_app(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st) {
+  // techniques the runtime rejects for an app are not instantiated
   switch (p.tech) {
-    case HPAC_TECH_TAF: return launch_tech<App, HPAC_TECH_TAF>(p, nblocks, smem, st);
-    case HPAC_TECH_IACT: return launch_tech<App, HPAC_TECH_IACT>(p, nblocks, smem, st);
+    case HPAC_TECH_TAF:
+      if constexpr (App::HAS_TAF) return launch_tech<App, HPAC_TECH_TAF>(p, nblocks, smem, st);
+      return cudaErrorInvalidValue;
+    case HPAC_TECH_IACT:
+      if constexpr (App::HAS_IACT) return launch_tech<App, HPAC_TECH_IACT>(p, nblocks, smem, st);
+      return cudaErrorInvalidValue;
     case HPAC_TECH_PERFO: return launch_tech<App, HPAC_TECH_PERFO>(p, nblocks, smem, st);
     default: return launch_tech<App, kTechNone>(p, nblocks, smem, st);
   }
