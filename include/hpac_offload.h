@@ -299,9 +299,11 @@ int hpac_mcr(const int32_t* accurate, const int32_t* approximate, int64_t n, voi
 
 /* ---- roofline support ------------------------------------------------- */
 /* Measured FP64 (DFMA) throughput of this device in TFLOP/s: MEASURED_PEAKS.json
-   carries HBM and bf16 peaks only, and every region here is FP64 CUDA-core
-   work, so the FP64 roofline denominator is measured in-run by this probe. */
+   carries HBM and bf16 peaks only, and the regions here compute in FP64, so
+   the FP64 roofline denominators are measured in-run by these probes. */
 int hpac_probe_fp64_peak(double* tflops);
+/* FP64 tensor-op (DMMA m8n8k4) peak, TFLOP/s: the K-Means DMMA filter's roofline. */
+int hpac_probe_dmma_peak(double* tflops);
 
 #ifdef __cplusplus
 }

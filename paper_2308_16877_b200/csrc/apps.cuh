@@ -45,6 +45,12 @@ struct AppBase {
     return p.region.encounters ? p.region.encounters[idx] : 1;
   }
   __device__ static void round_begin(const EngineParams&, int64_t, int, double*, bool, bool) {}
+  // warp-cooperative evaluation (EngineParams::warp_eval): called by all 32
+  // lanes of a hardware warp, converged; `want` = this lane evaluates
+  static constexpr bool WARP_EVAL = false;
+  __device__ static double warp_eval(const EngineParams&, int64_t, bool, const double*, int) {
+    return 0.0;
+  }
 };
 
 // Generic pure region over a work index (HPAC_APP_TABLE): load_input reads
@@ -146,6 +152,7 @@ struct AppKmeans : AppBase {
   static constexpr int IN_MAX = 32;
   static constexpr int OUT_MAX = 1;
   __device__ static void init(const EngineParams& p, double* scratch) {
+    if (p.warp_eval) return;  // warp_eval reads the per-launch km_aux block (L1-resident)
     const int k = p.region.kmeans_k, dims = p.region.kmeans_dims;
     const int kd = k * dims;
     for (int i = threadIdx.x; i < kd; i += blockDim.x) scratch[i] = p.region.centroids[i];
@@ -307,6 +314,160 @@ struct AppKmeans : AppBase {
   }
   __device__ static void store(const EngineParams& p, int64_t idx, const double (&out)[OUT_MAX], int) {
     if (p.region.labels) p.region.labels[idx] = (int32_t)out[0];
+  }
+};
+
+// (smallest, runner-up, argmin) update with one candidate, as predicated
+// selects (strict <: ties keep the earlier candidate; NaN never enters)
+__device__ __forceinline__ void top2_update(double e, int c, double& m1, double& m2, int& best) {
+  asm("{\n\t.reg .pred p0, p1;\n\t.reg .f64 t;\n\t"
+      "setp.lt.f64 p0, %3, %0;\n\t"
+      "setp.lt.f64 p1, %3, %1;\n\t"
+      "selp.f64 t, %3, %1, p1;\n\t"
+      "selp.f64 %1, %0, t, p0;\n\t"
+      "selp.f64 %0, %3, %0, p0;\n\t"
+      "selp.s32 %2, %4, %2, p0;\n\t}"
+      : "+d"(m1), "+d"(m2), "+r"(best)
+      : "d"(e), "r"(c));
+}
+
+// K-Means region with the warp-cooperative DMMA filter (EngineParams::warp_eval
+// set by the runtime for its shape); load/eval/store as AppKmeans.
+struct AppKmeansDmma : AppKmeans {
+#ifndef HPAC_KMD_MINB
+#define HPAC_KMD_MINB 4
+#endif
+  static constexpr int MIN_BLOCKS_256 = HPAC_KMD_MINB;
+  // Warp-cooperative filtered argmin on the FP64 tensor op (dims == 32,
+  // k % 8 == 0, no distance output; host-gated). The 32 items of a hardware
+  // warp are consecutive (per-thread mapping), so the warp computes the
+  // 32 x k block of x.c products as 4 x (k/8) m8n8k4 tiles over 8 k-steps.
+  // The reduction index is permuted (k-step s, slot t <-> dimension 8(s/2) + 2t + s%2)
+  // so every lane's operands are 16-byte pairs: points come straight from
+  // HBM as 2 KB coalesced rows per m-tile, centroids from a fragment-ordered
+  // copy (each 16-byte load contiguous across the warp, each element read
+  // once per warp instead of once per lane; a per-launch block prepared by
+  // kmeans_dmma_aux_kernel, L1-resident, so CTAs stage nothing). Each operand
+  // feeds 4 FMAs from registers, which lifts the shared-memory operand bound
+  // of eval() above.
+  // The estimate is certified exactly as in eval(): the bound E covers any
+  // summation order of the 32 products, so the label is the reference's.
+  static constexpr bool WARP_EVAL = true;
+#ifndef HPAC_KM_MT
+#define HPAC_KM_MT 1
+#endif
+#ifndef HPAC_KM_KS
+#define HPAC_KM_KS 1
+#endif
+  __device__ static double warp_eval(const EngineParams& p, int64_t idx, bool want,
+                                     const double*, int lane) {
+    const int k = p.region.kmeans_k;
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t base = idx - lane;  // item of lane 0
+    const unsigned wm = __ballot_sync(0xffffffffu, want);
+    const double* cc = p.km_aux + k * IN_MAX;  // norms [k], max norm
+    const double2* bf = reinterpret_cast<const double2*>(p.km_aux) + lane;
+    const double G = 4.0 * (4.0 * IN_MAX + 8.0) * 0x1.0p-53;
+    constexpr int MT = HPAC_KM_MT;  // m-tiles (8 points each) per pass
+    int mine = 0;
+#pragma unroll 1
+    for (int m0 = 0; m0 < 4; m0 += MT) {
+      if (!((wm >> (8 * m0)) & ((1ull << (8 * MT)) - 1))) continue;  // no point of this pass
+      double a[MT][8], xx[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int src = 8 * (m0 + i) + g;
+        if ((wm >> src) & 1u) {
+          // k-step s of slot t <-> dimension 8(s/2) + 2t + s%2: 64 contiguous
+          // bytes per (row, chunk) across the group's four lanes
+          const double2* x =
+              reinterpret_cast<const double2*>(p.region.in + (base + src) * IN_MAX) + t;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 v = __ldg(x + 4 * q);
+            a[i][2 * q] = v.x;
+            a[i][2 * q + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < 8; ++s) a[i][s] = 0.0;
+        }
+        double ss = 0.0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) ss = fma(a[i][s], a[i][s], ss);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        xx[i] = ss + __shfl_xor_sync(0xffffffffu, ss, 2);
+      }
+      double m1[MT], m2[MT];
+      int best[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        m1[i] = m2[i] = dinf();
+        best[i] = 0;
+      }
+      for (int j = 0; j < k; j += 8) {
+        double b[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 v = __ldg(bf + (j / 2 + q) * 32);  // (j/8 * 4 + q) * 32
+          b[2 * q] = v.x;
+          b[2 * q + 1] = v.y;
+        }
+        // KS independent accumulation chains per m-tile (k-steps s mod KS)
+        constexpr int KS = HPAC_KM_KS;
+        double acc[MT][KS][2];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int u = 0; u < KS; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+#pragma unroll
+          for (int i = 0; i < MT; ++i)
+            dmma_m8n8k4(acc[i][s % KS][0], acc[i][s % KS][1], a[i][s], b[s]);
+        const int c0 = j + 2 * t;
+        const double n0 = __ldg(cc + c0), n1 = __ldg(cc + c0 + 1);
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          double dot0 = acc[i][0][0], dot1 = acc[i][0][1];
+#pragma unroll
+          for (int u = 1; u < KS; ++u) {
+            dot0 += acc[i][u][0];
+            dot1 += acc[i][u][1];
+          }
+          // non-finite data never passes: E below is then inf/NaN
+          top2_update(fma(-2.0, dot0, xx[i] + n0), c0, m1[i], m2[i], best[i]);
+          top2_update(fma(-2.0, dot1, xx[i] + n1), c0 + 1, m1[i], m2[i], best[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        // merge the four lanes of the group (each saw 2 of every 8 centroids)
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+          const double o1 = __shfl_xor_sync(0xffffffffu, m1[i], off);
+          const double o2 = __shfl_xor_sync(0xffffffffu, m2[i], off);
+          const int ob = __shfl_xor_sync(0xffffffffu, best[i], off);
+          if (o1 < m1[i] || (o1 == m1[i] && ob < best[i])) {
+            m2[i] = fmin(m1[i], o2);
+            m1[i] = o1;
+            best[i] = ob;
+          } else {
+            m2[i] = fmin(m2[i], o1);
+          }
+        }
+        // cc[k] = max norm, NaN when any centroid is non-finite: E then
+        // fails the test and the point takes the reference path; so does a
+        // non-finite point (|x|^2 = inf/NaN) and any overflowing estimate
+        const double E = G * (xx[i] + __ldg(cc + k));
+        const int code = (m2[i] - m1[i] > 2.0 * E + 16.0 * 0x1.0p-53 * fabs(m2[i])) ? best[i] : -1;
+        // point L's result sits in lanes 4(L%8) .. +3 of m-tile L/8
+        const int v = __shfl_sync(0xffffffffu, code, 4 * (lane & 7));
+        if ((lane >> 3) == m0 + i) mine = v;
+      }
+    }
+    if (want && mine < 0) mine = exact_argmin_reload(p, idx, p.region.centroids);
+    return (double)mine;
   }
 };
 

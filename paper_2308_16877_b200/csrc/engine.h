@@ -49,6 +49,8 @@ struct EngineParams {
   int32_t has_enc, barrier_eval, accumulate;
   int32_t per_team;  // lane-level engine under per-team mapping (all lanes share idx)
   int32_t staged;    // app stages shared data per round (AppLavaMD)
+  int32_t warp_eval; // app evaluates a hardware warp's items cooperatively (AppKmeans DMMA)
+  const double* km_aux;  // AppKmeans warp_eval: DMMA B fragments [k*32], norms [k], max norm
   // shared-memory carve-up (doubles unless noted)
   int32_t smem_taf_off;   // TAF ring (smem variant)
   int32_t smem_last_off;  // TAF last (smem variant)

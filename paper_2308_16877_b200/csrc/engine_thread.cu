@@ -231,6 +231,18 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) e
       if (p.staged)
         App::round_begin(p, idx, round, smem + p.smem_scratch_off, active, in_round && !approx);
 
+      // ---- warp-cooperative evaluation (AppKmeans DMMA): the hardware warp
+      // evaluates its lanes' items together, converged, before the per-lane
+      // bookkeeping below consumes the results
+      double wout = 0.0;
+      if constexpr (App::WARP_EVAL) {  // launched only with p.warp_eval
+        bool want = in_round && !approx;
+        // iACT forced approximation with an empty table falls back (below)
+        if (TECH == HPAC_TECH_IACT && in_round && approx && hit < 0 && occ <= 0) want = true;
+        if (__any_sync(0xffffffffu, want))
+          wout = App::warp_eval(p, idx, want, smem + p.smem_scratch_off, hw_lane);
+      }
+
       // ---- lane execution (engine.hpp:303-347) -----------------------------
       double out[OUT_MAX];
 #pragma unroll
@@ -262,8 +274,12 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) e
           // perforation: output untouched
         }
         if (!approx) {
-          if (!loaded) App::load(p, idx, in);
-          if (!App::eval(p, idx, in, out, smem + p.smem_scratch_off, local, round)) app_error = true;
+          if constexpr (App::WARP_EVAL) {
+            out[0] = wout;
+          } else {
+            if (!loaded) App::load(p, idx, in);
+            if (!App::eval(p, idx, in, out, smem + p.smem_scratch_off, local, round)) app_error = true;
+          }
           if (p.barrier_eval) arrivals += 1;
           App::store(p, idx, out, local);
           if (TECH == HPAC_TECH_TAF) {
@@ -530,7 +546,7 @@ size_t engine_thread_smem(EngineParams& p) {
     off += (size_t)p.tsize * (p.in_dims + p.out_dims) * p.wpt * p.tpw;
   off = (off + 1) & ~(size_t)1;  // 16-byte aligned scratch (vector staging)
   p.smem_scratch_off = (int)off;
-  if (p.region.app == HPAC_APP_KMEANS)  // centroids + squared norms
+  if (p.region.app == HPAC_APP_KMEANS && !p.warp_eval)  // centroids + squared norms
     off += (size_t)p.region.kmeans_k * p.region.kmeans_dims + p.region.kmeans_k + 1;
   if (p.region.app == HPAC_APP_LAVAMD) off += (size_t)p.region.lavamd_particles * 5;
   p.smem_ctl_off = (int)off;
@@ -562,8 +578,51 @@ int engine_thread_max_out(int app) {
   return 0;
 }
 
+// Per-launch K-Means DMMA operand block (AppKmeans::warp_eval): B fragments
+// [(j*4 + m)*32 + L] (double2) = c[8j + L/4][8m + 2(L%4) .. +1], then the
+// squared norms (dimension-order fma, as AppKmeans::init) and their maximum.
+__global__ void kmeans_dmma_aux_kernel(const double* __restrict__ cent, int k, double* aux) {
+  double2* bf = reinterpret_cast<double2*>(aux);
+  for (int e = threadIdx.x; e < k * 16; e += blockDim.x) {
+    const int L = e & 31, m = (e >> 5) & 3, j = e >> 7;
+    const double* src = cent + (8 * j + (L >> 2)) * 32 + 8 * m + 2 * (L & 3);
+    bf[e] = make_double2(src[0], src[1]);
+  }
+  double* cc = aux + k * 32;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    double s = 0.0;
+    for (int d = 0; d < 32; ++d) s = fma(cent[c * 32 + d], cent[c * 32 + d], s);
+    cc[c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // max norm; NaN if any centroid is non-finite (warp_eval then certifies
+    // nothing and every point takes the reference path)
+    double mx = 0.0;
+    bool finite = true;
+    for (int c = 0; c < k; ++c) {
+      finite = finite && isfinite(cc[c]);
+      mx = fmax(mx, cc[c]);
+    }
+    cc[k] = finite ? mx : __longlong_as_double(0x7ff8000000000000ll);
+  }
+}
+
 cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem,
                                  cudaStream_t st) {
+  if (p.region.app == HPAC_APP_KMEANS && p.warp_eval) {
+    const int k = p.region.kmeans_k;
+    double* aux = nullptr;
+    cudaError_t e = cudaMallocAsync(&aux, ((size_t)k * 33 + 1) * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    kmeans_dmma_aux_kernel<<<1, 256, 0, st>>>(p.region.centroids, k, aux);
+    EngineParams q = p;
+    q.km_aux = aux;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = launch_app<AppKmeansDmma>(q, nblocks, smem, st);
+    cudaError_t f = cudaFreeAsync(aux, st);
+    return e != cudaSuccess ? e : f;
+  }
   switch (p.region.app) {
     case HPAC_APP_TABLE: return launch_app<AppTable>(p, nblocks, smem, st);
     case HPAC_APP_SYNTHETIC: return launch_app<AppSynthetic>(p, nblocks, smem, st);

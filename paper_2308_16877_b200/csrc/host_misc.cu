@@ -97,7 +97,60 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters
   if (s == 1.2345) sink[0] = s;
 }
 
+// Independent FP64 tensor-op (DMMA m8n8k4) chains: 8 per warp.
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* sink, int iters, double a, double b) {
+  double d[8][2];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) d[u][0] = d[u][1] = threadIdx.x + u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dmma_m8n8k4(d[u][0], d[u][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += d[u][0] + d[u][1];
+  if (s == 1.2345) sink[0] = s;
+}
+
 }  // namespace hpac
+
+namespace {
+template <class K>
+int probe_peak(K kernel, int blocks_per_sm, int iters, double flops_per_thread_iter, double* tflops) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HPAC_ERR_CUDA;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* sink;
+  if (cudaMalloc(&sink, 8) != cudaSuccess) return HPAC_ERR_CUDA;
+  const int blocks = sms * blocks_per_sm, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  kernel<<<blocks, threads>>>(sink, 64, 0.999999, 1e-7);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (cudaGetLastError() != cudaSuccess) return HPAC_ERR_CUDA;
+  *tflops = flops_per_thread_iter * iters * (double)blocks * threads / (best * 1e-3) / 1e12;
+  return HPAC_OK;
+}
+}  // namespace
+
+// FP64 tensor-op peak (the K-Means DMMA filter's roofline): 8 chains of
+// m8n8k4 (512 flops per warp-instruction = 16 per thread) per warp.
+HPAC_API int hpac_probe_dmma_peak(double* tflops) {
+  return probe_peak(hpac::dmma_probe_kernel, 4, 1024, 8.0 * 16.0, tflops);
+}
 
 HPAC_API int hpac_probe_fp64_peak(double* tflops) {
   int dev = 0, sms = 0;

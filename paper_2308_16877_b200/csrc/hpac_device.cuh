@@ -215,6 +215,15 @@ __device__ __forceinline__ bool taf_ring_passes_fixed(const double* ring, int st
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
 
+// FP64 tensor-core MMA, D = A(8x4, row) * B(4x8, col) + D, one warp. Lane L
+// holds A[L/4][L%4], B[L%4][L/4] and D[L/4][2(L%4)], D[L/4][2(L%4)+1].
+// (tcgen05 has no FP64 kind; the sm_80+ DMMA path is the FP64 tensor op.)
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // Writer key for the iACT max-min selection (iact.hpp:166-180): larger
 // distance wins, ties to the lower lane. Non-candidates carry d = -1.
 __device__ __forceinline__ bool writer_better(double da, int la, double db, int lb) {

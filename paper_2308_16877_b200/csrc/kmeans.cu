@@ -52,8 +52,14 @@ __global__ void kmeans_init_labels(int32_t* dist_label, int32_t* assign, int64_t
 // the 32 rows (lane = dimension, 256 B per row) with kBatch row loads in
 // flight before accumulating them, in point order, into the warp's private
 // shared-memory sums. Counts are integers (exact in any order).
-constexpr int kBatch = 32;
-__global__ void __launch_bounds__(kUpdWarps * 32)
+#ifndef HPAC_UPD_BATCH
+#define HPAC_UPD_BATCH 32
+#endif
+#ifndef HPAC_UPD_CTAS
+#define HPAC_UPD_CTAS 2
+#endif
+constexpr int kBatch = HPAC_UPD_BATCH;
+__global__ void __launch_bounds__(kUpdWarps * 32, HPAC_UPD_CTAS)
     kmeans_update_partial(const double* __restrict__ pts, const int32_t* __restrict__ dist_label,
                           int32_t* __restrict__ assign, int64_t n, int dims, int k, int64_t chunk,
                           double* __restrict__ part) {
@@ -201,7 +207,7 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int nparts = sms * 2;
+  const int nparts = sms * HPAC_UPD_CTAS;
   const int64_t warps = (int64_t)nparts * kUpdWarps;
   const int64_t chunk = n > 0 ? (n + warps - 1) / warps : 1;
   auto cleanup = [&]() {

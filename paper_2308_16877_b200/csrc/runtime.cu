@@ -390,6 +390,15 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
     pr.kind = 0;
     pr.block = p.tpt;
     pr.nblocks = te - tb;
+    // K-Means filtered argmin on the FP64 tensor op (AppKmeans::warp_eval)
+    // for its shape: 32 dims, k % 8 == 0, labels only, whole hardware warps;
+    // HPAC_KM_DMMA=0 keeps the per-lane CUDA-core filter (A/B tests)
+    if (r.app == HPAC_APP_KMEANS) {
+      const char* km = getenv("HPAC_KM_DMMA");
+      p.warp_eval = r.kmeans_dims == 32 && r.kmeans_k % 8 == 0 && !r.out &&
+                    !(r.flags & HPAC_REGION_KMEANS_FAST_MATH) && p.tpt % 32 == 0 && p.tpt <= 256 &&
+                    (reinterpret_cast<uintptr_t>(r.in) & 15) == 0 && !(km && strcmp(km, "0") == 0);
+    }
     pr.smem = engine_thread_smem(p);
     // streaming variant (bulk-TMA staged inputs) where it applies;
     // HPAC_ENGINE=thread forces the generic engine (A/B parity tests)
