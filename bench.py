@@ -768,6 +768,7 @@ def kmeans_lloyd_arm(args, wl):
                              perfo_seed_base=7, allreduce=allreduce, stream=stream)
             h_lab.copy_(r.assignments, non_blocking=True)
             its += r.iterations
+
         ev1.record(stream)
         torch.cuda.synchronize()
         e2e_t = ev0.elapsed_time(ev1)

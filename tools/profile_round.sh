@@ -37,6 +37,6 @@ cap binomial_exact 'binomial_team_kernel<.int.3' 0 --steps 1 --warmup 1
 cap bs_taf 'bs_stream_kernel<.int.0' 0 --workload blackscholes --steps 1 --warmup 1
 cap bs_exact 'bs_stream_kernel<.int.3' 0 --workload blackscholes --steps 1 --warmup 1
 cap lavamd_taf 'engine_thread_kernel<hpac::AppLavaMD, .int.0' 0 --workload lavamd --steps 1 --warmup 1
-cap kmeans_region 'engine_thread_kernel<hpac::AppKmeans, .int.2' 3 --workload kmeans --steps 1 --warmup 1
+cap kmeans_region 'engine_thread_kernel<hpac::AppKmeansDmma, .int.2' 3 --workload kmeans --steps 1 --warmup 1
 cap kmeans_update 'kmeans_update_partial' 3 --workload kmeans --steps 1 --warmup 1
 ls -la $O
