@@ -321,6 +321,7 @@ struct KmeansResult {
   bool converged = false;
   KernelStats stats;
   double region_ms = 0.0, update_ms = 0.0;
+  bool graph = false;  // the iterations ran as one CUDA graph launch
 };
 
 inline KmeansResult kmeans_benchmark(const double* points, long long n, int dims, int k,
@@ -349,6 +350,7 @@ inline KmeansResult kmeans_benchmark(const double* points, long long n, int dims
                r.stats.total_warp_steps};
   out.region_ms = r.region_ms;
   out.update_ms = r.update_ms;
+  out.graph = r.graph != 0;
   return out;
 }
 

@@ -247,7 +247,8 @@ typedef struct hpac_kmeans_problem {
                            the first k points (kmeans.hpp:66-71); out: final */
   int32_t* assignments; /* device, n labels (out) */
   int32_t max_iters;
-  int32_t flags;        /* HPAC_REGION_KMEANS_FAST_MATH | HPAC_KMEANS_CENTROIDS_GIVEN */
+  int32_t flags;        /* HPAC_REGION_KMEANS_FAST_MATH | HPAC_KMEANS_CENTROIDS_GIVEN |
+                           HPAC_KMEANS_HOST_LOOP */
   uint64_t perfo_seed_base; /* RANDOM perforation: seed of iteration i = base + i */
   hpac_allreduce_fn allreduce;
   void* allreduce_user;
@@ -255,6 +256,11 @@ typedef struct hpac_kmeans_problem {
 } hpac_kmeans_problem_t;
 
 #define HPAC_KMEANS_CENTROIDS_GIVEN 8
+/* Drive the loop from the host, one synchronised iteration at a time. By
+   default (no all-reduce hook) the whole loop is ONE CUDA graph launch: a
+   conditional WHILE node whose body is one iteration, with convergence
+   decided on the device (no host round trip per iteration). */
+#define HPAC_KMEANS_HOST_LOOP 16
 
 typedef struct hpac_kmeans_result {
   int32_t iterations;  /* region launches executed */
@@ -262,6 +268,7 @@ typedef struct hpac_kmeans_result {
   hpac_stats_t stats;  /* summed over launches */
   double region_ms;    /* device time in the distance region kernels */
   double update_ms;    /* device time in the centroid update kernels */
+  int32_t graph;       /* 1: the iterations ran as one CUDA graph launch */
 } hpac_kmeans_result_t;
 
 int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_t* problem,

@@ -79,6 +79,7 @@ class Launch(C.Structure):
 
 ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 KMEANS_CENTROIDS_GIVEN = 8
+KMEANS_HOST_LOOP = 16
 
 
 class KmeansProblem(C.Structure):
@@ -91,7 +92,7 @@ class KmeansProblem(C.Structure):
 
 class KmeansResult(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("stats", Stats),
-                ("region_ms", C.c_double), ("update_ms", C.c_double)]
+                ("region_ms", C.c_double), ("update_ms", C.c_double), ("graph", C.c_int32)]
 
 
 def _declare(lib):

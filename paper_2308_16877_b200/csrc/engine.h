@@ -51,6 +51,8 @@ struct EngineParams {
   int32_t staged;    // app stages shared data per round (AppLavaMD)
   int32_t warp_eval; // app evaluates a hardware warp's items cooperatively (AppKmeans DMMA)
   const double* km_aux;  // AppKmeans warp_eval: DMMA B fragments [k*32], norms [k], max norm
+                         // (preallocated by a captured Lloyd loop; else per launch)
+  const unsigned long long* seed_ptr;  // device perforation seed (captured loops); null = perfo_seed
   // shared-memory carve-up (doubles unless noted)
   int32_t smem_taf_off;   // TAF ring (smem variant)
   int32_t smem_last_off;  // TAF last (smem variant)

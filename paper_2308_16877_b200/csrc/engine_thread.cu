@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) e
 
   // ---- perforation counters (engine.hpp:70-71) -----------------------------
   int64_t pcount = 0, hcount = 0;
+  const uint64_t perfo_seed = p.seed_ptr ? (uint64_t)*p.seed_ptr : p.perfo_seed;
   int64_t trip = 0;
   if (TECH == HPAC_TECH_PERFO &&
       (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) e
         } else if (TECH == HPAC_TECH_PERFO) {
           const bool herded = p.perfo_kind == HPAC_PERFO_HERDED_SMALL ||
                               p.perfo_kind == HPAC_PERFO_HERDED_LARGE;
-          pred = perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed,
+          pred = perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, perfo_seed,
                                    herded ? hcount : pcount, trip, owner);
         }
       }
@@ -578,6 +579,8 @@ int engine_thread_max_out(int app) {
   return 0;
 }
 
+size_t kmeans_aux_bytes(int k) { return ((size_t)k * 33 + 1) * sizeof(double); }
+
 // Per-launch K-Means DMMA operand block (AppKmeans::warp_eval): B fragments
 // [(j*4 + m)*32 + L] (double2) = c[8j + L/4][8m + 2(L%4) .. +1], then the
 // squared norms (dimension-order fma, as AppKmeans::init) and their maximum.
@@ -612,14 +615,15 @@ cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem
                                  cudaStream_t st) {
   if (p.region.app == HPAC_APP_KMEANS && p.warp_eval) {
     const int k = p.region.kmeans_k;
-    double* aux = nullptr;
-    cudaError_t e = cudaMallocAsync(&aux, ((size_t)k * 33 + 1) * sizeof(double), st);
-    if (e != cudaSuccess) return e;
+    double* aux = const_cast<double*>(p.km_aux);  // preallocated (captured loop)
+    cudaError_t e = cudaSuccess;
+    if (!aux && (e = cudaMallocAsync(&aux, kmeans_aux_bytes(k), st)) != cudaSuccess) return e;
     kmeans_dmma_aux_kernel<<<1, 256, 0, st>>>(p.region.centroids, k, aux);
     EngineParams q = p;
     q.km_aux = aux;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = launch_app<AppKmeansDmma>(q, nblocks, smem, st);
+    if (p.km_aux) return e;
     cudaError_t f = cudaFreeAsync(aux, st);
     return e != cudaSuccess ? e : f;
   }

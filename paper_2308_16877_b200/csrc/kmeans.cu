@@ -164,10 +164,58 @@ __global__ void kmeans_reduce_partials(const double* part, int nparts, int width
 // centroids[c] = sums[c] / counts[c]; empty clusters keep theirs (kmeans.hpp:142-143)
 __global__ void kmeans_recompute(const double* red, int dims, int k, double* cent) {
   const int kd = k * dims;
+  if (red[kd + k] == 0.0) return;  // converged: centroids stay (kmeans.hpp:122-127)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kd; i += gridDim.x * blockDim.x) {
     double cnt = red[kd + i / dims];
     if (cnt > 0.0) cent[i] = red[i] / cnt;
   }
+}
+
+// ---- captured Lloyd loop (one CUDA graph: a device-side while loop) -------
+int region_prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_t* region,
+                   const hpac_spec_t* spec, unsigned long long* d_counters,
+                   const unsigned long long* seed_ptr, const double* km_aux, void** handle,
+                   char* err, size_t el);
+cudaError_t region_launch(const void* handle, cudaStream_t st);
+void region_free(void* handle);
+size_t kmeans_aux_bytes(int k);
+
+// Device state of a captured run: the region counters accumulate across
+// iterations; times are %globaltimer deltas (ns) between the marks.
+struct LoopState {
+  unsigned long long cnt[kNumCounters];
+  unsigned long long seed;  // perforation seed of the next iteration
+  int iter;                 // iterations run inside the graph
+  int converged;
+  unsigned long long t_mark, t_region, t_update;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void loop_mark(LoopState* s) { s->t_mark = globaltimer(); }
+__global__ void loop_after_region(LoopState* s) {
+  const unsigned long long t = globaltimer();
+  s->t_region += t - s->t_mark;
+  s->t_mark = t;
+}
+// End of an iteration: count it, key the next seed, and continue while some
+// label changed and iterations remain (kmeans.hpp:122-127)
+__global__ void loop_cond(LoopState* s, const double* changed, int iters_left, uint64_t seed_next0,
+                          cudaGraphConditionalHandle h) {
+  s->t_update += globaltimer() - s->t_mark;
+  const int it = ++s->iter;
+  s->seed = seed_next0 + (uint64_t)it;
+  bool more = true;
+  if (*changed == 0.0) {
+    s->converged = 1;
+    more = false;
+  } else if (it >= iters_left) {
+    more = false;
+  }
+  cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
 }  // namespace hpac
@@ -244,9 +292,113 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
   hpac_launch_t L{};
   L.stream = st;
   L.synchronous = 1;
+
+  // iterations first+1 .. max_iters inside one graph launch; returns
+  // kGraphUnavailable (nothing ran) when the body cannot be captured or
+  // instantiated, e.g. an all-reduce that is not stream-capturable
+  constexpr int kGraphUnavailable = -1;
+  auto run_graph = [&](int first) -> int {
+    const int left = pb->max_iters - first;
+    LoopState* ds = nullptr;
+    double* aux = nullptr;
+    void* hreg = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int grc = HPAC_OK;
+    LoopState hs{};
+    hs.cnt[kCntBarrierKey] = ~0ull;
+    hs.seed = pb->perfo_seed_base + (uint64_t)first + 1;
+    auto done = [&](int code) {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      if (cs) cudaStreamDestroy(cs);
+      if (hreg) region_free(hreg);
+      if (ds) cudaFreeAsync(ds, st);
+      if (aux) cudaFreeAsync(aux, st);
+      return code;
+    };
+    cudaError_t ge;
+    if ((ge = cudaMallocAsync(&ds, sizeof(LoopState), st)) != cudaSuccess ||
+        (ge = cudaMallocAsync(&aux, kmeans_aux_bytes(k), st)) != cudaSuccess ||
+        (ge = cudaMemcpyAsync(ds, &hs, sizeof hs, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return done(kfail(err, el, HPAC_ERR_CUDA, "kmeans graph alloc: %s", cudaGetErrorString(ge)));
+    grc = region_prepare(grid, n, HPAC_MAP_PER_THREAD, &r, spec, ds->cnt, &ds->seed, aux, &hreg,
+                         err, el);
+    if (grc) return done(grc);
+    cudaGraphConditionalHandle h;
+    cudaGraphNodeParams cp{};
+    cudaGraphNode_t node;
+    if ((ge = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess ||
+        (ge = cudaGraphCreate(&graph, 0)) != cudaSuccess ||
+        (ge = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault)) !=
+            cudaSuccess)
+      return done(kGraphUnavailable);
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if ((ge = cudaGraphAddNode(&node, graph, nullptr, 0, &cp)) != cudaSuccess)
+      return done(kGraphUnavailable);
+    // the loop body: one Lloyd iteration, captured
+    if ((ge = cudaStreamBeginCaptureToGraph(cs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+      return done(kGraphUnavailable);
+    loop_mark<<<1, 1, 0, cs>>>(ds);
+    ge = region_launch(hreg, cs);
+    loop_after_region<<<1, 1, 0, cs>>>(ds);
+    kmeans_update_partial<<<nparts, kUpdWarps * 32, upd_smem, cs>>>(
+        pb->points, dist_label, pb->assignments, n, dims, k, chunk, part);
+    kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, cs>>>(part, nparts,
+                                                                              (int)(stride + 1), red);
+    if (pb->allreduce) pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, cs);
+    kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, cs>>>(red, dims, k, pb->centroids);
+    loop_cond<<<1, 1, 0, cs>>>(ds, red + stride, left, pb->perfo_seed_base + (uint64_t)first + 1, h);
+    cudaGraph_t body;
+    cudaError_t ce = cudaStreamEndCapture(cs, &body);
+    if (ge == cudaSuccess) ge = ce;
+    if (ge == cudaSuccess) ge = cudaGetLastError();
+    if (ge != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      cudaGetLastError();  // capture errors are not sticky: clear and fall back
+      return done(kGraphUnavailable);
+    }
+    if ((ge = cudaGraphLaunch(exec, st)) != cudaSuccess ||
+        (ge = cudaMemcpyAsync(&hs, ds, sizeof hs, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (ge = cudaStreamSynchronize(st)) != cudaSuccess)
+      return done(kfail(err, el, HPAC_ERR_CUDA, "kmeans graph run: %s", cudaGetErrorString(ge)));
+    res->iterations = first + hs.iter;
+    res->converged = hs.converged;
+    res->graph = 1;
+    res->stats.total_invocations += hs.cnt[kCntTotal];
+    res->stats.approx_invocations += hs.cnt[kCntApprox];
+    res->stats.divergent_warp_steps += hs.cnt[kCntDivergent];
+    res->stats.total_warp_steps += hs.cnt[kCntWarpSteps];
+    if (hs.iter > 0) res->stats.resident_warps = (int32_t)(hs.cnt[kCntResidentWarps] / hs.iter);
+    res->region_ms += hs.t_region * 1e-6;
+    res->update_ms += hs.t_update * 1e-6;
+    return done(HPAC_OK);
+  };
   int rc = HPAC_OK;
   double h_changed = 0.0;
+  // The whole loop runs as one CUDA graph (a conditional while node: no
+  // host round trip per iteration) unless the caller's all-reduce hook is a
+  // host callback (only no hook or the native NCCL hook are captured), or
+  // HPAC_KMEANS_HOST_LOOP is set.
+  // RANDOM perforation's exact first iteration runs on the host path.
+  const bool random_perfo = spec && spec->technique == HPAC_TECH_PERFO &&
+                            spec->perfo_kind == HPAC_PERFO_RANDOM;
+  bool use_graph = (!pb->allreduce || pb->allreduce == hpac_nccl_allreduce) &&
+                   !(pb->flags & HPAC_KMEANS_HOST_LOOP) && n > 0;
+  const int graph_start = random_perfo ? 2 : 1;
   for (int iter = 1; iter <= pb->max_iters; ++iter) {
+    if (use_graph && iter == graph_start) {
+      const int g = run_graph(iter - 1);
+      if (g != kGraphUnavailable) {
+        rc = g;
+        break;
+      }
+      use_graph = false;  // not capturable here: the host drives the rest
+    }
     if (spec && spec->technique == HPAC_TECH_PERFO && spec->perfo_kind == HPAC_PERFO_RANDOM)
       sp.perfo_seed = pb->perfo_seed_base + (uint64_t)iter;
     hpac_stats_t s{};

@@ -475,6 +475,34 @@ int finish_status(const unsigned long long* c, hpac_stats_t* st, int app, char* 
 
 }  // namespace
 
+// Internal handles for captured loops (the K-Means Lloyd graph, kmeans.cu):
+// the region is validated once, then launched from inside a CUDA graph with
+// caller-owned counters (accumulating across iterations), a device seed and
+// a preallocated DMMA operand block.
+namespace hpac {
+int region_prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_t* region,
+                   const hpac_spec_t* spec, unsigned long long* d_counters,
+                   const unsigned long long* seed_ptr, const double* km_aux, void** handle,
+                   char* err, size_t el) {
+  Prepared* pr = new Prepared;
+  hpac_stats_t st{};
+  int rc = prepare(g, n, mapping, region, spec, nullptr, *pr, &st, err, el);
+  if (rc) {
+    delete pr;
+    return rc;
+  }
+  pr->p.counters = d_counters;
+  pr->p.seed_ptr = seed_ptr;
+  pr->p.km_aux = km_aux;
+  *handle = pr;
+  return HPAC_OK;
+}
+cudaError_t region_launch(const void* handle, cudaStream_t st) {
+  return launch_prepared(*static_cast<const Prepared*>(handle), st);
+}
+void region_free(void* handle) { delete static_cast<Prepared*>(handle); }
+}  // namespace hpac
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================

@@ -355,16 +355,19 @@ class KmeansResult:
     stats: dict
     region_ms: float
     update_ms: float
+    graph: bool = False  # the iterations ran as one CUDA graph launch
 
 
 def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=None,
                fast_math=False, perfo_seed_base=0, allreduce=None, stream=None,
-               nccl_comm=None) -> KmeansResult:
+               nccl_comm=None, host_loop=False) -> KmeansResult:
     """kmeans_benchmark (bench/kmeans.hpp:62-144) on the device. `points` is a
     torch CUDA tensor n x d. `allreduce(buf_tensor)` (optional) all-reduces the
     packed [sums | counts | changed] partials across ranks each iteration;
     `nccl_comm` (an ncclComm_t handle) uses the library's native NCCL hook
-    (hpac_nccl_allreduce) instead."""
+    (hpac_nccl_allreduce) instead. Without a hook the loop runs as one CUDA
+    graph launch (device-side convergence); host_loop=True forces one
+    synchronised host round trip per iteration."""
     import torch
     n, d = points.shape
     cent = torch.empty((k, d), dtype=torch.float64, device=points.device) if centroids is None else centroids
@@ -375,7 +378,8 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
     pb.points, pb.centroids, pb.assignments = _ptr(points), _ptr(cent), _ptr(assign)
     pb.max_iters = max_iters
     pb.flags = (abi.REGION_KMEANS_FAST_MATH if fast_math else 0) | \
-        (abi.KMEANS_CENTROIDS_GIVEN if centroids is not None else 0)
+        (abi.KMEANS_CENTROIDS_GIVEN if centroids is not None else 0) | \
+        (abi.KMEANS_HOST_LOOP if host_loop else 0)
     pb.perfo_seed_base = perfo_seed_base
     pb.reduce_buf = _ptr(red)
     cb = None
@@ -396,7 +400,7 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
     if rc:
         _raise(rc, err, res.stats)
     return KmeansResult(assign, cent, res.iterations, bool(res.converged), res.stats.as_dict(),
-                        res.region_ms, res.update_ms)
+                        res.region_ms, res.update_ms, bool(res.graph))
 
 
 def nccl_comms(ndev=1):

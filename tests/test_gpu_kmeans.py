@@ -109,7 +109,40 @@ def test_native_nccl_allreduce_hook():
         a = E.kmeans_run(grid, dev(pts), 16, E.perfo("random", 25, seed=3), max_iters=20, perfo_seed_base=5)
         b = E.kmeans_run(grid, dev(pts), 16, E.perfo("random", 25, seed=3), max_iters=20, perfo_seed_base=5,
                          nccl_comm=comm)
+        # the hook inside the captured loop (or its host-loop fallback) and
+        # the host-driven loop agree
+        c = E.kmeans_run(grid, dev(pts), 16, E.perfo("random", 25, seed=3), max_iters=20, perfo_seed_base=5,
+                         nccl_comm=comm, host_loop=True)
     finally:
         abi.lib().hpac_nccl_comm_destroy(C.c_void_p(comm))
-    assert a.iterations == b.iterations
-    assert torch.equal(a.assignments, b.assignments) and torch.equal(a.centroids, b.centroids)
+    print("nccl hook captured in the graph:", b.graph)
+    for r in (b, c):
+        assert a.iterations == r.iterations
+        assert torch.equal(a.assignments, r.assignments) and torch.equal(a.centroids, r.centroids)
+
+
+@pytest.mark.parametrize("n,d,k,sep,spec_fn,iters", [
+    (8192, 32, 64, 30.0, lambda: None, 40),
+    (8192, 32, 64, 8.0, lambda: None, 7),
+    (4096, 2, 8, 8.0, lambda: E.perfo("small", 4), 40),
+    (8192, 32, 64, 30.0, lambda: E.perfo("random", 52, level="team"), 40),
+    (8192, 32, 64, 8.0, lambda: E.perfo("random", 30, level="warp"), 12),
+    (4096, 2, 8, 8.0, lambda: E.iact(4, 0.0, 1), 40),
+    (512, 2, 4, 14.0, lambda: None, 1),
+])
+def test_graph_loop_equals_host_loop(n, d, k, sep, spec_fn, iters):
+    """The CUDA-graph Lloyd loop (conditional WHILE node, device-side
+    convergence, device perforation seed) runs the same kernels in the same
+    order as the host-driven loop: identical labels, centroids (bitwise),
+    iteration count, convergence and stats."""
+    pts = dev(E.make_blobs(n, d, k, 5, sep))
+    grid, _ = E.resolve_grid("kmeans", n)
+    g = E.kmeans_run(grid, pts, k, spec_fn(), max_iters=iters, perfo_seed_base=3)
+    h = E.kmeans_run(grid, pts, k, spec_fn(), max_iters=iters, perfo_seed_base=3, host_loop=True)
+    assert g.graph and not h.graph
+    assert (g.iterations, g.converged) == (h.iterations, h.converged)
+    assert torch.equal(g.assignments, h.assignments)
+    assert torch.equal(g.centroids, h.centroids)
+    for key in ("total_invocations", "approx_invocations", "divergent_warp_steps", "total_warp_steps"):
+        assert g.stats[key] == h.stats[key], key
+    assert g.region_ms > 0 and g.update_ms > 0
