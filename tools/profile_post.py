@@ -32,6 +32,7 @@ METRICS = [
     ("dram_pct", "dram__cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
     ("fp64_pipe_pct", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", 1),
     ("alu_pipe_pct", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", 1),
+    ("dmma_pipe_pct", "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", 1),
     ("issue_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active", 1),
     ("threads_per_inst", "smsp__thread_inst_executed_per_inst_executed.ratio", 1),
     ("divergent_branch_targets", "smsp__sass_branch_targets_threads_divergent.sum", 1),
@@ -78,9 +79,9 @@ def read_raw(path):
 def main(tag):
     PROF.mkdir(exist_ok=True)
     lines = [f"# Profile round {tag} (B200, ncu --set full --clock-control none, one launch each)", "",
-             "| capture | kernel | µs | DRAM MB (r+w) | DRAM GB/s | DRAM % | FP64 pipe % | ALU % | issue % | "
+             "| capture | kernel | µs | DRAM MB (r+w) | DRAM GB/s | DRAM % | FP64 pipe % | DMMA pipe % | ALU % | issue % | "
              "warp exec eff | divergent branch targets | occupancy % | regs | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = json.loads((PROF / "traffic.json").read_text()) if (PROF / "traffic.json").exists() else {}
     for name, wl in CAPTURES.items():
         raw = OUT / f"{tag}_{name}_raw.csv"
@@ -93,7 +94,8 @@ def main(tag):
         us = r.get("duration_us") or 0
         gbs = byt / (us * 1e-6) / 1e9 if us else 0
         lines.append(f"| {name} | `{r['kernel'][:60]}` | {us:.1f} | {byt / 1e6:.1f} | {gbs:.0f} | "
-                     f"{r.get('dram_pct', 0):.1f} | {r.get('fp64_pipe_pct', 0):.1f} | {r.get('alu_pipe_pct', 0):.1f} | "
+                     f"{r.get('dram_pct', 0):.1f} | {r.get('fp64_pipe_pct', 0):.1f} | {r.get('dmma_pipe_pct', 0):.1f} | "
+                     f"{r.get('alu_pipe_pct', 0):.1f} | "
                      f"{r.get('issue_pct', 0):.1f} | {r.get('threads_per_inst', 0) / 32:.3f} | "
                      f"{r.get('divergent_branch_targets', 0):.0f} | {r.get('occupancy_pct', 0):.1f} | "
                      f"{r.get('registers', 0):.0f} | {r['top_stalls']} |")
