@@ -359,6 +359,9 @@ struct AppKmeansDmma : AppKmeans {
 #ifndef HPAC_KM_KS
 #define HPAC_KM_KS 1
 #endif
+#ifndef HPAC_KM_PF
+#define HPAC_KM_PF 1
+#endif
   __device__ static double warp_eval(const EngineParams& p, int64_t idx, bool want,
                                      const double*, int lane) {
     const int k = p.region.kmeans_k;
@@ -372,6 +375,16 @@ struct AppKmeansDmma : AppKmeans {
     int mine = 0;
 #pragma unroll 1
     for (int m0 = 0; m0 < 4; m0 += MT) {
+#if HPAC_KM_PF
+      // L1 prefetch of the rows the next pass loads (after the last pass:
+      // the first rows of this thread's next step), one 128-byte line per
+      // lane, so their HBM latency overlaps this pass's DMMAs
+      if (lane < 16 * MT) {
+        const int64_t row = (m0 + MT < 4 ? base + 8 * (m0 + MT) : base + p.stride) + (lane >> 1);
+        if (row < p.n)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p.region.in + row * IN_MAX + (lane & 1) * 16));
+      }
+#endif
       if (!((wm >> (8 * m0)) & ((1ull << (8 * MT)) - 1))) continue;  // no point of this pass
       double a[MT][8], xx[MT];
 #pragma unroll
