@@ -582,7 +582,7 @@ def our_arm(args, wl):
             h_out = torch.zeros(n, dtype=torch.float64).pin_memory()
             hreg = (E.binomial_region(h_in.numpy(), wl["lattice"], h_out.numpy())
                     if wl["benchmark"] == "binomial" else E.blackscholes_region(h_in.numpy(), h_out.numpy()))
-        E.run_region_host(grid, n, mapping, hreg, spec)  # warm-up
+        zc = E.run_region_host(grid, n, mapping, hreg, spec).stats["zero_copy"]  # warm-up
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
@@ -595,7 +595,10 @@ def our_arm(args, wl):
             e2e_t = t.item()
         e2e = {"value": ws * n * per_item * args.e2e_steps / e2e_t, "unit": wl["unit"],
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
-               "steps": args.e2e_steps}
+               "steps": args.e2e_steps,
+               "transfer": ("zero-copy: the region kernel reads the pinned host inputs and writes the "
+                            "pinned host outputs in place over PCIe" if zc else
+                            "staged: H2D copy, region kernel, D2H copy")}
 
     if rank != 0:
         if dist is not None:

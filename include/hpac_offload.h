@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define HPAC_ABI_VERSION 1
+#define HPAC_ABI_VERSION 2
 
 /* ---- status codes ------------------------------------------------------ */
 #define HPAC_OK 0
@@ -147,6 +147,10 @@ typedef struct hpac_stats {
      N(N+1)/2 per evaluated option; early-exercise tracking skips nodes whose
      value is the analytic exercise value) */
   uint64_t lattice_nodes;
+  /* hpac_run_region_host: 1 = the kernel read/wrote the caller's pinned
+     buffers in place (zero-copy), 0 = staged through device buffers */
+  int32_t zero_copy;
+  int32_t reserved0;
 } hpac_stats_t;
 
 /* Region descriptor (replaces engine.hpp:26-33). Pointers are caller-owned;
@@ -222,7 +226,11 @@ int hpac_run_region(const hpac_grid_t* grid, int64_t n, int32_t mapping,
                     size_t errlen);
 
 /* Same call with HOST buffers: copies inputs host->device, runs, copies
-   outputs device->host (the reference-facing end-to-end entry). */
+   outputs device->host (the reference-facing end-to-end entry). For the
+   stream-once regions (Blackscholes, the K-Means labels region) with
+   page-locked caller buffers the kernel reads and writes them in place
+   instead (zero-copy over PCIe/C2C, both directions overlapped with the
+   compute; stats->zero_copy = 1); HPAC_HOST_COPY=1 forces staging. */
 int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
                          const hpac_region_t* host_region, const hpac_spec_t* spec,
                          hpac_stats_t* stats, char* err, size_t errlen);

@@ -55,7 +55,7 @@ class Stats(C.Structure):
                 ("arena_required", C.c_uint64), ("arena_available", C.c_uint64),
                 ("fail_step", C.c_int64), ("fail_team", C.c_int32), ("fail_missing", C.c_int32),
                 ("kernel_ms", C.c_double), ("lattice_fallbacks", C.c_uint64),
-                ("lattice_nodes", C.c_uint64)]
+                ("lattice_nodes", C.c_uint64), ("zero_copy", C.c_int32), ("reserved0", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

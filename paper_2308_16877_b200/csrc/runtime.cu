@@ -66,6 +66,8 @@ struct Scratch {
   hpac_stats_t pending_base{};
 };
 thread_local Scratch g_scratch;
+// set by the zero-copy host entry around its launch: generic per-thread engine
+thread_local bool g_force_thread_engine = false;
 
 cudaError_t scratch_ready() {
   int dev = 0;
@@ -403,7 +405,8 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
     // streaming variant (bulk-TMA staged inputs) where it applies;
     // HPAC_ENGINE=thread forces the generic engine (A/B parity tests)
     const char* force = getenv("HPAC_ENGINE");
-    if (engine_stream_eligible(p) && !(force && strcmp(force, "thread") == 0)) {
+    if (engine_stream_eligible(p) && !(force && strcmp(force, "thread") == 0) &&
+        !g_force_thread_engine) {
       pr.kind = 3;
       pr.smem = engine_stream_smem(p);
     }
@@ -646,6 +649,17 @@ HPAC_API int hpac_stats_fetch(hpac_stats_t* stats) {
   return finish_status(g_scratch.h_cnt, stats, -1, buf, sizeof buf);
 }
 
+// Device-usable address of page-locked (pinned) host memory, else null.
+const void* pinned_device_ptr(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 // Private stream-ordered pool for the host-buffer entry: memory is kept
 // across calls (release threshold = max), so repeated end-to-end calls do
 // not re-map device memory every time (the default pool trims at syncs).
@@ -720,18 +734,40 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
     return d;
   };
   hpac_region_t d = r;
-  d.in = (const double*)dalloc(in_bytes, r.in, true);
-  d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true);
-  d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true);
-  // outputs start from the caller's contents (skipped items keep them)
-  d.out = (double*)dalloc(out_bytes, r.out, true);
-  d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true);
-  d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true);
+  // Zero-copy for the stream-once regions (Blackscholes; the K-Means labels
+  // region): when the caller's buffers are pinned, the kernel reads the
+  // inputs and writes the outputs over PCIe in place, so the host->device
+  // and device->host transfers overlap each other and the compute instead
+  // of running back to back. The generic per-thread engine is used: its
+  // independent per-lane loads keep more PCIe reads in flight than one bulk
+  // copy per team. HPAC_HOST_COPY=1 keeps the staged path.
+  const bool zc_app = r.app == HPAC_APP_BLACKSCHOLES || (r.app == HPAC_APP_KMEANS && !r.out);
+  const char* hc = getenv("HPAC_HOST_COPY");
+  const bool zero_copy = zc_app && !(hc && strcmp(hc, "1") == 0) && pinned_device_ptr(r.in) &&
+                         (!r.out || pinned_device_ptr(r.out)) &&
+                         (!r.labels || pinned_device_ptr(r.labels));
+  if (zero_copy) {
+    d.in = (const double*)pinned_device_ptr(r.in);
+    d.out = (double*)pinned_device_ptr(r.out);
+    d.labels = (int32_t*)pinned_device_ptr(r.labels);
+    d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true);  // read per CTA: stage
+  } else {
+    d.in = (const double*)dalloc(in_bytes, r.in, true);
+    d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true);
+    d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true);
+    // outputs start from the caller's contents (skipped items keep them)
+    d.out = (double*)dalloc(out_bytes, r.out, true);
+    d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true);
+    d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true);
+  }
   hpac_launch_t L{};
   L.stream = st;
   L.synchronous = 1;
+  g_force_thread_engine = zero_copy;
   rc = hpac_run_region(grid, n, mapping, &d, spec, &L, stats, err, el);
-  if (rc == HPAC_OK) {
+  g_force_thread_engine = false;
+  if (stats) stats->zero_copy = zero_copy ? 1 : 0;
+  if (rc == HPAC_OK && !zero_copy) {
     if (out_bytes) cudaMemcpyAsync(r.out, d.out, out_bytes, cudaMemcpyDeviceToHost, st);
     if (lab_bytes) cudaMemcpyAsync(r.labels, d.labels, lab_bytes, cudaMemcpyDeviceToHost, st);
   }
