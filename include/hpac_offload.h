@@ -240,9 +240,10 @@ int hpac_stats_fetch(hpac_stats_t* stats);
 
 /* ---- K-Means Lloyd loop (bench/kmeans.hpp:62-144) ---------------------- */
 /* Sum-reduction hook for the per-iteration centroid partials: a packed
-   device buffer [k*dims sums | k counts | 1 changed] (doubles). Multi-GPU
-   callers all-reduce it across ranks (e.g. ncclAllReduce / torch
-   all_reduce over NCCL); NULL = single device. */
+   device buffer [k*dims sum changes | k count changes | 1 changed] (doubles;
+   the iteration's moves: +x into a point's new cluster, -x out of its old
+   one). Multi-GPU callers all-reduce it across ranks (e.g. ncclAllReduce /
+   torch all_reduce over NCCL); NULL = single device. */
 typedef void (*hpac_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
 
 typedef struct hpac_kmeans_problem {

@@ -9,12 +9,14 @@
 // that argmin ("dist label", initialised to 0 = argmin of the zero-filled
 // distance matrix) instead of n*k doubles.
 //
-// Centroid update: one warp per contiguous chunk of points, lane = dimension
-// (coalesced 256 B rows), per-warp private shared-memory accumulators (no
-// atomics), then a fixed-order reduction (deterministic run to run). The
-// packed [sums | counts | changed] buffer is the only cross-GPU exchange; the
-// caller's all-reduce hook (NCCL) runs between the partial sums and the
-// centroid recompute.
+// Centroid update: running per-cluster sums and counts, changed by the
+// points whose label changed this iteration (+x into the new cluster, -x out
+// of the old one). One warp per contiguous chunk of points, lane = dimension
+// (coalesced 256 B rows of the changed points only), per-warp private
+// shared-memory accumulators (no atomics), then a fixed-order reduction
+// (deterministic run to run). The packed [sum deltas | count deltas |
+// changed] buffer is the only cross-GPU exchange; the caller's all-reduce
+// hook (NCCL) runs between the partial sums and the centroid recompute.
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -46,23 +48,63 @@ __global__ void kmeans_init_labels(int32_t* dist_label, int32_t* assign, int64_t
   }
 }
 
-// Per-CTA partials: [k*dims sums | k counts | changed] into part[cta][...].
-// A warp walks its contiguous chunk 32 points at a time: lane j reads point
-// j's label and updates its assignment (coalesced), then the warp streams
-// the 32 rows (lane = dimension, 256 B per row) with kBatch row loads in
-// flight before accumulating them, in point order, into the warp's private
-// shared-memory sums. Counts are integers (exact in any order).
-#ifndef HPAC_UPD_BATCH
-#define HPAC_UPD_BATCH 32
-#endif
-#ifndef HPAC_UPD_CTAS
-#define HPAC_UPD_CTAS 2
-#endif
-constexpr int kBatch = HPAC_UPD_BATCH;
-__global__ void __launch_bounds__(kUpdWarps * 32, HPAC_UPD_CTAS)
+// The iteration's label changes, compacted per sub-chunk in point order
+// (deterministic): sub-chunk g = points [g*sub, (g+1)*sub), one warp each,
+// 4 batches of 32 labels in flight. Changed points are listed with their old
+// assignment, and their assignment is updated (kmeans.hpp:122-127).
+constexpr int kCompactU = 4;
+__global__ void __launch_bounds__(256)
+    kmeans_changed_compact(const int32_t* __restrict__ dist_label, int32_t* __restrict__ assign,
+                           int64_t n, int64_t sub, int64_t nsub, int32_t* __restrict__ list,
+                           int32_t* __restrict__ oldlab, int32_t* __restrict__ list_len) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gs = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gs >= nsub) return;
+  const int64_t lo = gs * sub, hi = lo + sub < n ? lo + sub : n;
+  int cnt = 0;
+  for (int64_t b0 = lo; b0 < hi; b0 += 32 * kCompactU) {
+    int nl[kCompactU], ol[kCompactU];
+#pragma unroll
+    for (int u = 0; u < kCompactU; ++u) {
+      const int64_t i = b0 + u * 32 + lane;
+      nl[u] = i < hi ? __ldcs(dist_label + i) : 0;
+      ol[u] = i < hi ? assign[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kCompactU; ++u) {
+      const int64_t i = b0 + u * 32 + lane;
+      const bool ch = i < hi && nl[u] != ol[u];
+      const unsigned m = __ballot_sync(0xffffffffu, ch);
+      if (ch) {
+        const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+        list[lo + pos] = (int32_t)(i - lo);
+        oldlab[lo + pos] = ol[u];
+        assign[i] = nl[u];
+      }
+      cnt += __popc(m);
+    }
+  }
+  if (lane == 0) list_len[gs] = cnt;
+}
+
+// Per-CTA partials of the iteration's CHANGES: [k*dims sum deltas | k count
+// deltas | changed] into part[cta][...]. Only points whose label changed
+// move: + x into the new cluster, - x out of the old one (none on the first
+// iteration, where every assignment is -1). The running sums (kmeans_accumulate)
+// therefore always equal the sum of every point under its current label,
+// the reference's full re-sum (kmeans.hpp:133-141) up to rounding, while an
+// iteration reads the labels and assignments (8 B per point) plus the rows
+// of the changed points only. Warp w walks the compacted lists of its
+// sub-chunks in order, 32 entries at a time: lane j reads entry j (index,
+// old and new label); the changed rows (lane = dimension, 256 B per row) of
+// group g+1 are in flight while group g accumulates, in point order, into
+// the warp's private shared-memory sums. Count deltas are integers.
+constexpr int kBatch = 32;
+__global__ void __launch_bounds__(kUpdWarps * 32, 2)
     kmeans_update_partial(const double* __restrict__ pts, const int32_t* __restrict__ dist_label,
-                          int32_t* __restrict__ assign, int64_t n, int dims, int k, int64_t chunk,
-                          double* __restrict__ part) {
+                          const int32_t* __restrict__ list, const int32_t* __restrict__ oldlab,
+                          const int32_t* __restrict__ list_len, int64_t sub, int subs_per_warp,
+                          int64_t nsub, int dims, int k, double* __restrict__ part) {
   extern __shared__ __align__(16) double acc[];  // [warps][k*dims] then int counts [warps][k]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int kd = k * dims;
@@ -72,58 +114,76 @@ __global__ void __launch_bounds__(kUpdWarps * 32, HPAC_UPD_CTAS)
   for (int i = lane; i < k; i += 32) cnts[i] = 0;
   __syncwarp();
   const int64_t gw = (int64_t)blockIdx.x * kUpdWarps + w;
-  const int64_t lo = gw * chunk, hi = lo + chunk < n ? lo + chunk : n;
   unsigned long long changed = 0;
-  if (dims <= 32) {
-    // software-pipelined: batch b+1's rows and labels are in flight while
-    // batch b is accumulated
-    const bool dl = lane < dims;
-    double xa[kBatch], xb[kBatch];
-    int la = 0, lb = 0;
-    auto fetch = [&](int64_t b0, double (&x)[kBatch], int& lab) {
-      const int cnt = (int)(hi - b0 < kBatch ? hi - b0 : kBatch);
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j)
-        x[j] = (j < cnt && dl) ? __ldcs(pts + (b0 + j) * dims + lane) : 0.0;
-      lab = lane < cnt ? dist_label[b0 + lane] : 0;
+  const bool dl = lane < dims;
+  for (int64_t gs = gw * subs_per_warp; gs < (gw + 1) * subs_per_warp && gs < nsub; ++gs) {
+    const int64_t lo = gs * sub;
+    const int len = list_len[gs];
+    changed += len;
+    // lane j of group e0: entry e0 + j (point, new label, old label)
+    auto entry = [&](int e0, int64_t& pi, int& nl, int& ol) {
+      const bool v = e0 + lane < len;
+      pi = v ? lo + list[lo + e0 + lane] : 0;
+      nl = v ? dist_label[pi] : 0;
+      ol = v ? oldlab[lo + e0 + lane] : -1;
     };
-    if (lo < hi) fetch(lo, xa, la);
-    for (int64_t b0 = lo; b0 < hi; b0 += kBatch) {
-      const int cnt = (int)(hi - b0 < kBatch ? hi - b0 : kBatch);
-      if (b0 + kBatch < hi) fetch(b0 + kBatch, xb, lb);
-      if (lane < cnt) {
-        if (assign[b0 + lane] != la) {
-          ++changed;
-          assign[b0 + lane] = la;
-        }
-        atomicAdd(&cnts[la], 1);
-      }
+    if (dims <= 32) {
+      double xa[kBatch], xb[kBatch];
+      int64_t pa = 0, pb = 0;
+      int na = 0, oa = -1, nb = 0, ob = -1;
+      auto fetch = [&](int e0, double (&x)[kBatch], int64_t& pi, int& nl, int& ol) {
+        entry(e0, pi, nl, ol);
+        const int c = len - e0 < kBatch ? len - e0 : kBatch;
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
-        const int c = __shfl_sync(0xffffffffu, la, j);
-        if (j < cnt && dl) my[(size_t)c * dims + lane] += xa[j];
-      }
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j) xa[j] = xb[j];
-      la = lb;
-    }
-  } else {
-    for (int64_t base = lo; base < hi; base += 32) {
-      const int cnt = (int)(hi - base < 32 ? hi - base : 32);
-      int c_l = 0;
-      if (lane < cnt) {
-        c_l = dist_label[base + lane];
-        if (assign[base + lane] != c_l) {
-          ++changed;
-          assign[base + lane] = c_l;
+        for (int j = 0; j < kBatch; ++j) {
+          const int64_t pj = __shfl_sync(0xffffffffu, pi, j);
+          x[j] = (j < c && dl) ? __ldcs(pts + pj * dims + lane) : 0.0;
         }
-        atomicAdd(&cnts[c_l], 1);
+      };
+      if (len > 0) fetch(0, xa, pa, na, oa);
+      for (int e0 = 0; e0 < len; e0 += kBatch) {
+        const int c = len - e0 < kBatch ? len - e0 : kBatch;
+        if (e0 + kBatch < len) fetch(e0 + kBatch, xb, pb, nb, ob);
+        if (lane < c) {
+          atomicAdd(&cnts[na], 1);
+          if (oa >= 0) atomicSub(&cnts[oa], 1);
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+          if (j >= c) break;
+          const int cn = __shfl_sync(0xffffffffu, na, j), co = __shfl_sync(0xffffffffu, oa, j);
+          if (dl) {
+            my[(size_t)cn * dims + lane] += xa[j];
+            if (co >= 0) my[(size_t)co * dims + lane] -= xa[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) xa[j] = xb[j];
+        pa = pb;
+        na = nb;
+        oa = ob;
       }
-      for (int j = 0; j < cnt; ++j) {
-        const int c = __shfl_sync(0xffffffffu, c_l, j);
-        for (int d = lane; d < dims; d += 32) my[(size_t)c * dims + d] += __ldcs(pts + (base + j) * dims + d);
+    } else {
+      for (int e0 = 0; e0 < len; e0 += 32) {
+        int64_t pi;
+        int nl, ol;
+        entry(e0, pi, nl, ol);
+        const int c = len - e0 < 32 ? len - e0 : 32;
+        if (lane < c) {
+          atomicAdd(&cnts[nl], 1);
+          if (ol >= 0) atomicSub(&cnts[ol], 1);
+        }
+        for (int j = 0; j < c; ++j) {
+          const int64_t pj = __shfl_sync(0xffffffffu, pi, j);
+          const int cn = __shfl_sync(0xffffffffu, nl, j), co = __shfl_sync(0xffffffffu, ol, j);
+          for (int d = lane; d < dims; d += 32) {
+            const double x = __ldcs(pts + pj * dims + d);
+            my[(size_t)cn * dims + d] += x;
+            if (co >= 0) my[(size_t)co * dims + d] -= x;
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   __syncthreads();
@@ -142,8 +202,7 @@ __global__ void __launch_bounds__(kUpdWarps * 32, HPAC_UPD_CTAS)
     out[kd + j] = (double)s;
   }
   __shared__ unsigned long long ch[kUpdWarps];
-  const unsigned long long wsum = __reduce_add_sync(0xffffffffu, (unsigned)changed);
-  if (lane == 0) ch[w] = wsum;
+  if (lane == 0) ch[w] = changed;  // identical in every lane
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
@@ -161,13 +220,25 @@ __global__ void kmeans_reduce_partials(const double* part, int nparts, int width
   }
 }
 
+// Running sums and counts += this iteration's (all-reduced) changes; an
+// emptied cluster's sums restart from exact zero.
+__global__ void kmeans_accumulate(const double* red, int dims, int k, double* tot) {
+  const int kd = k * dims;
+  if (red[kd + k] == 0.0) return;  // converged: nothing moved
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kd + k; i += gridDim.x * blockDim.x) {
+    const int c = i < kd ? i / dims : i - kd;
+    const double cnt = tot[kd + c] + red[kd + c];  // exact: integers below 2^53
+    tot[i] = i < kd ? (cnt > 0.0 ? tot[i] + red[i] : 0.0) : cnt;
+  }
+}
+
 // centroids[c] = sums[c] / counts[c]; empty clusters keep theirs (kmeans.hpp:142-143)
-__global__ void kmeans_recompute(const double* red, int dims, int k, double* cent) {
+__global__ void kmeans_recompute(const double* red, const double* tot, int dims, int k, double* cent) {
   const int kd = k * dims;
   if (red[kd + k] == 0.0) return;  // converged: centroids stay (kmeans.hpp:122-127)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kd; i += gridDim.x * blockDim.x) {
-    double cnt = red[kd + i / dims];
-    if (cnt > 0.0) cent[i] = red[i] / cnt;
+    const double cnt = tot[kd + i / dims];
+    if (cnt > 0.0) cent[i] = tot[i] / cnt;
   }
 }
 
@@ -179,6 +250,9 @@ int region_prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_
 cudaError_t region_launch(const void* handle, cudaStream_t st);
 void region_free(void* handle);
 size_t kmeans_aux_bytes(int k);
+}  // namespace hpac
+cudaMemPool_t host_entry_pool();  // runtime.cu: retained pool of the host entries
+namespace hpac {
 
 // Device state of a captured run: the region counters accumulate across
 // iterations; times are %globaltimer deltas (ns) between the marks.
@@ -252,20 +326,41 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
   int32_t* dist_label = nullptr;
   double* part = nullptr;
   double* red = pb->reduce_buf;
+  double* tot = nullptr;  // running [sums | counts] under the current labels
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int nparts = sms * HPAC_UPD_CTAS;
+  const int nparts = sms * 2;
   const int64_t warps = (int64_t)nparts * kUpdWarps;
-  const int64_t chunk = n > 0 ? (n + warps - 1) / warps : 1;
+  // sub-chunks: kSubsPerWarp per update warp, one compaction warp each
+  constexpr int kSubsPerWarp = 8;
+  const int64_t nsub = warps * kSubsPerWarp;
+  const int64_t sub = n > 0 ? (n + nsub - 1) / nsub : 1;
+  int32_t *list = nullptr, *oldlab = nullptr, *list_len = nullptr;
   auto cleanup = [&]() {
     if (dist_label) cudaFreeAsync(dist_label, st);
     if (part) cudaFreeAsync(part, st);
     if (red && red != pb->reduce_buf) cudaFreeAsync(red, st);
+    if (tot) cudaFreeAsync(tot, st);
+    if (list) cudaFreeAsync(list, st);
+    if (oldlab) cudaFreeAsync(oldlab, st);
+    if (list_len) cudaFreeAsync(list_len, st);
   };
-  if ((e = cudaMallocAsync(&dist_label, sizeof(int32_t) * (size_t)(n > 0 ? n : 1), st)) ||
-      (e = cudaMallocAsync(&part, sizeof(double) * (stride + 1) * nparts, st)) ||
-      (!red && (e = cudaMallocAsync(&red, sizeof(double) * (stride + 1), st)))) {
+  // run-scoped buffers from the library's retained stream-ordered pool (no
+  // re-mapping of ~200 MB of scratch on every run)
+  cudaMemPool_t pool = host_entry_pool();
+  auto palloc = [&](auto** ptr, size_t bytes) {
+    return pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, pool, st)
+                : cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, st);
+  };
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  if ((e = palloc(&dist_label, sizeof(int32_t) * nn)) ||
+      (e = palloc(&part, sizeof(double) * (stride + 1) * nparts)) ||
+      (!red && (e = palloc(&red, sizeof(double) * (stride + 1)))) ||
+      (e = palloc(&tot, sizeof(double) * stride)) || (e = palloc(&list, sizeof(int32_t) * nn)) ||
+      (e = palloc(&oldlab, sizeof(int32_t) * nn)) ||
+      (e = palloc(&list_len, sizeof(int32_t) * (size_t)nsub)) ||
+      (e = cudaMemsetAsync(tot, 0, sizeof(double) * stride, st))) {
     cleanup();
     return kfail(err, el, HPAC_ERR_CUDA, "kmeans alloc: %s", cudaGetErrorString(e));
   }
@@ -347,12 +442,15 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     loop_mark<<<1, 1, 0, cs>>>(ds);
     ge = region_launch(hreg, cs);
     loop_after_region<<<1, 1, 0, cs>>>(ds);
+    kmeans_changed_compact<<<(int)((nsub + 7) / 8), 256, 0, cs>>>(
+        dist_label, pb->assignments, n, sub, nsub, list, oldlab, list_len);
     kmeans_update_partial<<<nparts, kUpdWarps * 32, upd_smem, cs>>>(
-        pb->points, dist_label, pb->assignments, n, dims, k, chunk, part);
+        pb->points, dist_label, list, oldlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
     kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, cs>>>(part, nparts,
                                                                               (int)(stride + 1), red);
     if (pb->allreduce) pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, cs);
-    kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, cs>>>(red, dims, k, pb->centroids);
+    kmeans_accumulate<<<(int)((stride + 255) / 256), 256, 0, cs>>>(red, dims, k, tot);
+    kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, cs>>>(red, tot, dims, k, pb->centroids);
     loop_cond<<<1, 1, 0, cs>>>(ds, red + stride, left, pb->perfo_seed_base + (uint64_t)first + 1, h);
     cudaGraph_t body;
     cudaError_t ce = cudaStreamEndCapture(cs, &body);
@@ -423,8 +521,10 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     // labels -> assignments, change count, partial sums (every point, as the
     // reference sums all points in order, kmeans.hpp:135-141)
     cudaEventRecord(e0, st);
+    kmeans_changed_compact<<<(int)((nsub + 7) / 8), 256, 0, st>>>(
+        dist_label, pb->assignments, n, sub, nsub, list, oldlab, list_len);
     kmeans_update_partial<<<nparts, kUpdWarps * 32, upd_smem, st>>>(
-        pb->points, dist_label, pb->assignments, n, dims, k, chunk, part);
+        pb->points, dist_label, list, oldlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
     kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, st>>>(part, nparts,
                                                                               (int)(stride + 1), red);
     if ((e = cudaGetLastError()) != cudaSuccess) {
@@ -445,7 +545,8 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
       res->converged = 1;
       break;
     }
-    kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, st>>>(red, dims, k, pb->centroids);
+    kmeans_accumulate<<<(int)((stride + 255) / 256), 256, 0, st>>>(red, dims, k, tot);
+    kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, st>>>(red, tot, dims, k, pb->centroids);
   }
   res->stats.kernel_ms = res->region_ms + res->update_ms;
   cudaEventDestroy(e0);
