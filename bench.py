@@ -713,7 +713,16 @@ def kmeans_lloyd_arm(args, wl):
     cent0 = torch.from_numpy(E.make_blobs(n, d, k, 42, wl["separation"])[:k].copy() if rank else pts[:k].copy()).to(dev)
     grid, _ = E.resolve_grid("kmeans", n, items_per_thread=wl["ipt"])
     spec = make_spec(E, wl["spec"])
-    allreduce = D.kmeans_allreduce_hook() if dist is not None else None
+    # N > 1: the library's NCCL communicator, so the all-reduce is captured
+    # in the Lloyd loop's CUDA graph; torch.distributed's all_reduce as a
+    # host callback otherwise (BENCH_KMEANS_TORCH_HOOK=1 forces it)
+    allreduce, nccl_comm = None, None
+    if dist is not None:
+        if (not os.environ.get("BENCH_KMEANS_TORCH_HOOK")
+                and os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl"):
+            nccl_comm = D.native_nccl_comm(rank, ws)
+        if nccl_comm is None:
+            allreduce = D.kmeans_allreduce_hook()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     def one(sp, seed):
@@ -722,7 +731,7 @@ def kmeans_lloyd_arm(args, wl):
         torch.cuda.synchronize()
         flush.zero_()
         r = E.kmeans_run(grid, d_pts, k, sp, max_iters=wl["max_iters"], centroids=cent0.clone(),
-                         perfo_seed_base=seed, allreduce=allreduce, stream=stream)
+                         perfo_seed_base=seed, allreduce=allreduce, stream=stream, nccl_comm=nccl_comm)
         torch.cuda.synchronize()
         # device time of the run: the library's CUDA events around every
         # region launch and every update (partials + all-reduce + readback);
@@ -768,7 +777,7 @@ def kmeans_lloyd_arm(args, wl):
         for _ in range(args.e2e_steps):
             buf.copy_(h_pts, non_blocking=True)
             r = E.kmeans_run(grid, buf, k, spec, max_iters=wl["max_iters"], centroids=cent0.clone(),
-                             perfo_seed_base=7, allreduce=allreduce, stream=stream)
+                             perfo_seed_base=7, allreduce=allreduce, stream=stream, nccl_comm=nccl_comm)
             h_lab.copy_(r.assignments, non_blocking=True)
             its += r.iterations
 

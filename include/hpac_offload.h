@@ -289,6 +289,11 @@ int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_t* proble
    given stream. NCCL is loaded at run time (libnccl.so.2); 0 = unavailable. */
 int hpac_nccl_available(void);
 void hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream);
+/* Multi-process communicator for the hook (one process per GPU): rank 0
+   writes a 128-byte NCCL unique id, the caller broadcasts it, every rank
+   joins (ncclGetUniqueId / ncclCommInitRank). */
+int hpac_nccl_unique_id(uint8_t* id128);
+int hpac_nccl_comm_init_rank(int nranks, const uint8_t* id128, int rank, void** comm);
 /* ncclCommInitAll over `ndev` local devices (one process owning them all);
    comms receives ndev ncclComm_t handles. */
 int hpac_nccl_comm_init_all(int ndev, const int* devlist, void** comms);

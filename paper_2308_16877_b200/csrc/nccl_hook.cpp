@@ -14,6 +14,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 
 #include "hpac_offload.h"
@@ -25,6 +26,11 @@ typedef int (*AllReduceFn)(const void*, void*, size_t, int /*dtype*/, int /*op*/
                            void* /*stream*/);
 typedef int (*InitAllFn)(void** /*comms*/, int, const int*);
 typedef int (*DestroyFn)(void*);
+struct NcclUid {  // nccl.h ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128)
+  char internal[128];
+};
+typedef int (*GetUidFn)(NcclUid*);
+typedef int (*InitRankFn)(void** /*comm*/, int /*nranks*/, NcclUid /*id, by value*/, int /*rank*/);
 constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h ncclDataType_t / ncclRedOp_t
 
 struct Nccl {
@@ -32,6 +38,8 @@ struct Nccl {
   AllReduceFn all_reduce = nullptr;
   InitAllFn init_all = nullptr;
   DestroyFn destroy = nullptr;
+  GetUidFn get_uid = nullptr;
+  InitRankFn init_rank = nullptr;
 };
 
 Nccl* nccl() {
@@ -43,6 +51,8 @@ Nccl* nccl() {
     n.all_reduce = reinterpret_cast<AllReduceFn>(dlsym(n.h, "ncclAllReduce"));
     n.init_all = reinterpret_cast<InitAllFn>(dlsym(n.h, "ncclCommInitAll"));
     n.destroy = reinterpret_cast<DestroyFn>(dlsym(n.h, "ncclCommDestroy"));
+    n.get_uid = reinterpret_cast<GetUidFn>(dlsym(n.h, "ncclGetUniqueId"));
+    n.init_rank = reinterpret_cast<InitRankFn>(dlsym(n.h, "ncclCommInitRank"));
   });
   return n.all_reduce ? &n : nullptr;
 }
@@ -62,6 +72,27 @@ HPAC_API int hpac_nccl_comm_init_all(int ndev, const int* devlist, void** comms)
   Nccl* n = nccl();
   if (!n || !n->init_all) return HPAC_ERR_UNSUPPORTED;
   return n->init_all(comms, ndev, devlist) == 0 ? HPAC_OK : HPAC_ERR_CUDA;
+}
+
+// Multi-process communicators (one process per GPU, e.g. under torchrun):
+// rank 0 creates the 128-byte id, the caller broadcasts it (any channel),
+// every rank then joins. With this communicator as the hook's `user`, the
+// Lloyd loop's all-reduce is captured into its CUDA graph.
+HPAC_API int hpac_nccl_unique_id(uint8_t* id128) {
+  Nccl* n = nccl();
+  if (!n || !n->get_uid || !id128) return HPAC_ERR_UNSUPPORTED;
+  NcclUid id;
+  if (n->get_uid(&id) != 0) return HPAC_ERR_CUDA;
+  std::memcpy(id128, id.internal, sizeof id.internal);
+  return HPAC_OK;
+}
+
+HPAC_API int hpac_nccl_comm_init_rank(int nranks, const uint8_t* id128, int rank, void** comm) {
+  Nccl* n = nccl();
+  if (!n || !n->init_rank || !id128 || !comm) return HPAC_ERR_UNSUPPORTED;
+  NcclUid id;
+  std::memcpy(id.internal, id128, sizeof id.internal);
+  return n->init_rank(comm, nranks, id, rank) == 0 ? HPAC_OK : HPAC_ERR_CUDA;
 }
 
 HPAC_API int hpac_nccl_comm_destroy(void* comm) {

@@ -34,6 +34,22 @@ def kmeans_allreduce_hook(group=None):
     return hook
 
 
+def native_nccl_comm(rank: int, world: int):
+    """The library's own NCCL communicator across the torch.distributed ranks
+    (id broadcast over the default group), or None if NCCL is not loadable.
+    Passed as kmeans_run(nccl_comm=...), the Lloyd loop's all-reduce runs
+    inside its CUDA graph instead of a host callback per iteration."""
+    import torch.distributed as dist
+
+    from . import abi
+    from . import engine as E
+    if not abi.lib().hpac_nccl_available():
+        return None
+    obj = [E.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return E.nccl_comm_init_rank(world, obj[0], rank)
+
+
 def max_over_ranks(values, device=None, group=None):
     """Element-wise max of a list of floats across ranks (device-timed numbers
     are reported as the max over ranks)."""

@@ -413,6 +413,25 @@ def nccl_comms(ndev=1):
     return list(comms)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to broadcast to the other ranks."""
+    buf = C.create_string_buffer(128)
+    rc = abi.lib().hpac_nccl_unique_id(buf)
+    if rc:
+        raise UnsupportedError("NCCL unavailable") if rc == abi.ERR_UNSUPPORTED else CudaError("ncclGetUniqueId")
+    return buf.raw
+
+
+def nccl_comm_init_rank(nranks: int, uid: bytes, rank: int):
+    """Join a multi-process NCCL communicator (one process per GPU); the
+    handle is kmeans_run's `nccl_comm`."""
+    comm = C.c_void_p()
+    rc = abi.lib().hpac_nccl_comm_init_rank(nranks, uid, rank, C.byref(comm))
+    if rc:
+        raise UnsupportedError("NCCL unavailable") if rc == abi.ERR_UNSUPPORTED else CudaError("ncclCommInitRank")
+    return comm.value
+
+
 # ---- generators (host) -----------------------------------------------------
 
 def make_bs_portfolio(n, seed, base_block=512, jitter=0.01):

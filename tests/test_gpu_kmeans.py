@@ -146,3 +146,25 @@ def test_graph_loop_equals_host_loop(n, d, k, sep, spec_fn, iters):
     for key in ("total_invocations", "approx_invocations", "divergent_warp_steps", "total_warp_steps"):
         assert g.stats[key] == h.stats[key], key
     assert g.region_ms > 0 and g.update_ms > 0
+
+
+def test_native_nccl_comm_init_rank_single_process():
+    """hpac_nccl_unique_id + hpac_nccl_comm_init_rank (the multi-process
+    communicator bench.py uses under torchrun) with one rank: the Lloyd
+    loop with its all-reduce captured in the graph equals the hook-less run."""
+    if not abi.lib().hpac_nccl_available():
+        pytest.skip("libnccl.so.2 not loadable")
+    uid = E.nccl_unique_id()
+    assert len(uid) == 128
+    comm = E.nccl_comm_init_rank(1, uid, 0)
+    pts = E.make_blobs(8192, 32, 64, 4, 30.0)
+    grid, _ = E.resolve_grid("kmeans", 8192)
+    try:
+        a = E.kmeans_run(grid, dev(pts), 64, E.perfo("random", 40, level="team"), max_iters=15, perfo_seed_base=2)
+        b = E.kmeans_run(grid, dev(pts), 64, E.perfo("random", 40, level="team"), max_iters=15, perfo_seed_base=2,
+                         nccl_comm=comm)
+    finally:
+        abi.lib().hpac_nccl_comm_destroy(C.c_void_p(comm))
+    assert b.graph
+    assert a.iterations == b.iterations
+    assert torch.equal(a.assignments, b.assignments) and torch.equal(a.centroids, b.centroids)
