@@ -24,6 +24,7 @@ CAPTURES = {  # capture name -> bench workload whose timed kernel it is
     "lavamd_taf": "lavamd-64^3-boxes-x-128-taf-warp",
     "kmeans_region": "kmeans-lloyd-16M-x-32-x-64-perfo-random-team",
     "kmeans_update": None,
+    "kmeans_compact": None,
 }
 METRICS = [
     ("duration_us", "gpu__time_duration.sum", 1e-3),

@@ -39,4 +39,5 @@ cap bs_exact 'bs_stream_kernel<.int.3' 0 --workload blackscholes --steps 1 --war
 cap lavamd_taf 'engine_thread_kernel<hpac::AppLavaMD, .int.0' 0 --workload lavamd --steps 1 --warmup 1
 cap kmeans_region 'engine_thread_kernel<hpac::AppKmeansDmma, .int.2' 3 --workload kmeans --steps 1 --warmup 1
 cap kmeans_update 'kmeans_update_partial' 3 --workload kmeans --steps 1 --warmup 1
+cap kmeans_compact 'kmeans_changed_compact' 3 --workload kmeans --steps 1 --warmup 1
 ls -la $O
