@@ -17,11 +17,12 @@ timeout 900 $B --workload kmeans --steps 2 --warmup 1 > $O/${TAG}_bench_kmeans.j
 timeout 600 $B --workload kmeans-region --steps 5 --warmup 3 > $O/${TAG}_bench_kmeans-region.json 2> $O/${TAG}_bench_kmeans-region.err
 fi
 # ---- launch list of the default bench command (cold-cache, serialised: compare shares)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches_binomial.csv \
+[ -z "$CAPS" ] && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches_binomial.csv \
   $B --steps 2 --warmup 1 $Q > /dev/null 2>&1
 # ---- one full capture of each workload's timed kernel
-cap() {  # name, kernel regex, skip, bench args...
+cap() {  # name, kernel regex, skip, bench args...   (CAPS=regex: only matching names)
   local name=$1 rx=$2 skip=$3; shift 3
+  if [ -n "$CAPS" ] && ! [[ $name =~ $CAPS ]]; then return; fi
   timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     -k "regex:$rx" -s $skip -c 1 -o $O/${TAG}_$name -f $B "$@" $Q > $O/${TAG}_$name.log 2>&1
   ncu -i $O/${TAG}_$name.ncu-rep --page raw --csv > $O/${TAG}_${name}_raw.csv 2>/dev/null
@@ -37,7 +38,11 @@ cap binomial_exact 'binomial_team_kernel<.int.3' 0 --steps 1 --warmup 1
 cap bs_taf 'bs_stream_kernel<.int.0' 0 --workload blackscholes --steps 1 --warmup 1
 cap bs_exact 'bs_stream_kernel<.int.3' 0 --workload blackscholes --steps 1 --warmup 1
 cap lavamd_taf 'engine_thread_kernel<hpac::AppLavaMD, .int.0' 0 --workload lavamd --steps 1 --warmup 1
+# the Lloyd loop runs as a CUDA graph with a conditional node, whose kernel
+# nodes ncu cannot profile: capture the host-driven loop (same kernels)
+export HPAC_KMEANS_HOST_LOOP=1
 cap kmeans_region 'engine_thread_kernel<hpac::AppKmeansDmma, .int.2' 3 --workload kmeans --steps 1 --warmup 1
 cap kmeans_update 'kmeans_update_partial' 3 --workload kmeans --steps 1 --warmup 1
 cap kmeans_compact 'kmeans_changed_compact' 3 --workload kmeans --steps 1 --warmup 1
+unset HPAC_KMEANS_HOST_LOOP
 ls -la $O
