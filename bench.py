@@ -774,12 +774,25 @@ def kmeans_lloyd_arm(args, wl):
         its = 0
         torch.cuda.synchronize()
         ev0.record(stream)
+        dbg = os.environ.get("BENCH_DEBUG")
         for _ in range(args.e2e_steps):
+            t_0 = time.perf_counter()
             buf.copy_(h_pts, non_blocking=True)
+            if dbg:
+                torch.cuda.synchronize()
+                t_1 = time.perf_counter()
             r = E.kmeans_run(grid, buf, k, spec, max_iters=wl["max_iters"], centroids=cent0.clone(),
                              perfo_seed_base=7, allreduce=allreduce, stream=stream, nccl_comm=nccl_comm)
+            if dbg:
+                t_2 = time.perf_counter()
             h_lab.copy_(r.assignments, non_blocking=True)
             its += r.iterations
+            if dbg:
+                torch.cuda.synchronize()
+                t_3 = time.perf_counter()
+                print(f"e2e step: h2d {(t_1 - t_0) * 1e3:.1f} ms, lloyd {(t_2 - t_1) * 1e3:.1f} ms "
+                      f"(kernels {r.region_ms + r.update_ms:.1f}), d2h {(t_3 - t_2) * 1e3:.1f} ms",
+                      file=sys.stderr)
 
         ev1.record(stream)
         torch.cuda.synchronize()

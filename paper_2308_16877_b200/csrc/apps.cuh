@@ -356,12 +356,51 @@ struct AppKmeansDmma : AppKmeans {
 #ifndef HPAC_KM_MT
 #define HPAC_KM_MT 1
 #endif
-#ifndef HPAC_KM_KS
-#define HPAC_KM_KS 1
+#ifndef HPAC_KM_NT
+#define HPAC_KM_NT 2
 #endif
 #ifndef HPAC_KM_PF
 #define HPAC_KM_PF 1
 #endif
+  // NT n-tiles starting at centroid j against MT m-tiles: x.c by DMMA, then
+  // the (smallest, runner-up, argmin) update with this lane's 2 NT candidates
+  template <int NT, int MT>
+  __device__ __forceinline__ static void dmma_tiles(const double2* bf, const double* cc, int j, int t,
+                                                    const double (&a)[MT][8], const double (&xx)[MT],
+                                                    double (&m1)[MT], double (&m2)[MT], int (&best)[MT]) {
+    double b[NT][8];
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 v = __ldg(bf + ((j / 8 + u) * 4 + q) * 32);
+        b[u][2 * q] = v.x;
+        b[u][2 * q + 1] = v.y;
+      }
+    double acc[NT][MT][2];
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+#pragma unroll
+      for (int i = 0; i < MT; ++i) acc[u][i][0] = acc[u][i][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) dmma_m8n8k4(acc[u][i][0], acc[u][i][1], a[i][s], b[u][s]);
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+      const int c0 = j + 8 * u + 2 * t;
+      const double n0 = __ldg(cc + c0), n1 = __ldg(cc + c0 + 1);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        // non-finite data never passes: E in warp_eval is then inf/NaN
+        top2_update(fma(-2.0, acc[u][i][0], xx[i] + n0), c0, m1[i], m2[i], best[i]);
+        top2_update(fma(-2.0, acc[u][i][1], xx[i] + n1), c0 + 1, m1[i], m2[i], best[i]);
+      }
+    }
+  }
+
   __device__ static double warp_eval(const EngineParams& p, int64_t idx, bool want,
                                      const double*, int lane) {
     const int k = p.region.kmeans_k;
@@ -418,41 +457,12 @@ struct AppKmeansDmma : AppKmeans {
         m1[i] = m2[i] = dinf();
         best[i] = 0;
       }
-      for (int j = 0; j < k; j += 8) {
-        double b[8];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 v = __ldg(bf + (j / 2 + q) * 32);  // (j/8 * 4 + q) * 32
-          b[2 * q] = v.x;
-          b[2 * q + 1] = v.y;
-        }
-        // KS independent accumulation chains per m-tile (k-steps s mod KS)
-        constexpr int KS = HPAC_KM_KS;
-        double acc[MT][KS][2];
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int u = 0; u < KS; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
-#pragma unroll
-        for (int s = 0; s < 8; ++s)
-#pragma unroll
-          for (int i = 0; i < MT; ++i)
-            dmma_m8n8k4(acc[i][s % KS][0], acc[i][s % KS][1], a[i][s], b[s]);
-        const int c0 = j + 2 * t;
-        const double n0 = __ldg(cc + c0), n1 = __ldg(cc + c0 + 1);
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          double dot0 = acc[i][0][0], dot1 = acc[i][0][1];
-#pragma unroll
-          for (int u = 1; u < KS; ++u) {
-            dot0 += acc[i][u][0];
-            dot1 += acc[i][u][1];
-          }
-          // non-finite data never passes: E below is then inf/NaN
-          top2_update(fma(-2.0, dot0, xx[i] + n0), c0, m1[i], m2[i], best[i]);
-          top2_update(fma(-2.0, dot1, xx[i] + n1), c0 + 1, m1[i], m2[i], best[i]);
-        }
-      }
+      // NT n-tiles (8 centroids each) per step: NT independent accumulation
+      // chains per m-tile; a k % (8 NT) tail runs one n-tile at a time
+      int j = 0;
+      for (; j + 8 * HPAC_KM_NT <= k; j += 8 * HPAC_KM_NT)
+        dmma_tiles<HPAC_KM_NT, MT>(bf, cc, j, t, a, xx, m1, m2, best);
+      for (; j < k; j += 8) dmma_tiles<1, MT>(bf, cc, j, t, a, xx, m1, m2, best);
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         // merge the four lanes of the group (each saw 2 of every 8 centroids)

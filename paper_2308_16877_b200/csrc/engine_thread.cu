@@ -579,6 +579,10 @@ int engine_thread_max_out(int app) {
   return 0;
 }
 
+}  // namespace hpac
+cudaMemPool_t host_entry_pool();  // runtime.cu: the library's retained pool
+namespace hpac {
+
 size_t kmeans_aux_bytes(int k) { return ((size_t)k * 33 + 1) * sizeof(double); }
 
 // Per-launch K-Means DMMA operand block (AppKmeans::warp_eval): B fragments
@@ -617,7 +621,13 @@ cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem
     const int k = p.region.kmeans_k;
     double* aux = const_cast<double*>(p.km_aux);  // preallocated (captured loop)
     cudaError_t e = cudaSuccess;
-    if (!aux && (e = cudaMallocAsync(&aux, kmeans_aux_bytes(k), st)) != cudaSuccess) return e;
+    // per-launch block from the retained pool (no physical re-mapping inside
+    // the timed stream work); a captured loop passes its own
+    cudaMemPool_t pool = p.km_aux ? nullptr : host_entry_pool();
+    if (!aux && (e = pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&aux),
+                                                    kmeans_aux_bytes(k), pool, st)
+                          : cudaMallocAsync(&aux, kmeans_aux_bytes(k), st)) != cudaSuccess)
+      return e;
     kmeans_dmma_aux_kernel<<<1, 256, 0, st>>>(p.region.centroids, k, aux);
     EngineParams q = p;
     q.km_aux = aux;

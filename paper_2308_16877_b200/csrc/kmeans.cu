@@ -270,6 +270,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__global__ void loop_init(LoopState* s, uint64_t seed) {
+  for (int i = 0; i < kNumCounters; ++i) s->cnt[i] = i == kCntBarrierKey ? ~0ull : 0ull;
+  s->seed = seed;
+  s->iter = 0;
+  s->converged = 0;
+  s->t_mark = s->t_region = s->t_update = 0;
+}
 __global__ void loop_mark(LoopState* s) { s->t_mark = globaltimer(); }
 __global__ void loop_after_region(LoopState* s) {
   const unsigned long long t = globaltimer();
@@ -403,8 +410,6 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     cudaGraphExec_t exec = nullptr;
     int grc = HPAC_OK;
     LoopState hs{};
-    hs.cnt[kCntBarrierKey] = ~0ull;
-    hs.seed = pb->perfo_seed_base + (uint64_t)first + 1;
     auto done = [&](int code) {
       if (exec) cudaGraphExecDestroy(exec);
       if (graph) cudaGraphDestroy(graph);
@@ -415,9 +420,10 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
       return code;
     };
     cudaError_t ge;
-    if ((ge = cudaMallocAsync(&ds, sizeof(LoopState), st)) != cudaSuccess ||
-        (ge = cudaMallocAsync(&aux, kmeans_aux_bytes(k), st)) != cudaSuccess ||
-        (ge = cudaMemcpyAsync(ds, &hs, sizeof hs, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    if ((ge = palloc(&ds, sizeof(LoopState))) != cudaSuccess ||
+        (ge = palloc(&aux, kmeans_aux_bytes(k))) != cudaSuccess ||
+        (loop_init<<<1, 1, 0, st>>>(ds, pb->perfo_seed_base + (uint64_t)first + 1),
+         (ge = cudaGetLastError()) != cudaSuccess))
       return done(kfail(err, el, HPAC_ERR_CUDA, "kmeans graph alloc: %s", cudaGetErrorString(ge)));
     grc = region_prepare(grid, n, HPAC_MAP_PER_THREAD, &r, spec, ds->cnt, &ds->seed, aux, &hreg,
                          err, el);
