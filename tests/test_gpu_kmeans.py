@@ -168,3 +168,19 @@ def test_native_nccl_comm_init_rank_single_process():
     assert b.graph
     assert a.iterations == b.iterations
     assert torch.equal(a.assignments, b.assignments) and torch.equal(a.centroids, b.centroids)
+
+
+@pytest.mark.parametrize("host_loop", [False, True])
+def test_lloyd_run_to_run_deterministic(host_loop):
+    """Incremental centroid sums with fixed-order reductions: two runs on the
+    same inputs give bitwise-identical centroids, labels and stats."""
+    pts = dev(E.make_blobs(40000, 32, 64, 8, 12.0))
+    grid, _ = E.resolve_grid("kmeans", 40000)
+    spec = E.perfo("random", 40, level="warp")
+    runs = [E.kmeans_run(grid, pts, 64, spec, max_iters=25, perfo_seed_base=9, host_loop=host_loop)
+            for _ in range(2)]
+    a, b = runs
+    assert a.iterations == b.iterations and a.converged == b.converged
+    assert torch.equal(a.assignments, b.assignments)
+    assert torch.equal(a.centroids, b.centroids)
+    assert a.stats == b.stats
