@@ -353,6 +353,9 @@ struct AppKmeansDmma : AppKmeans {
   // The estimate is certified exactly as in eval(): the bound E covers any
   // summation order of the 32 products, so the label is the reference's.
   static constexpr bool WARP_EVAL = true;
+  // build-time tuning knobs (tools/build_variant.sh; A/B results in DESIGN
+  // §4.2): m-tiles per pass, n-tiles per step, L1 prefetch of the next rows,
+  // and HPAC_KMD_MINB above (CTAs of 256 threads per SM -> register cap)
 #ifndef HPAC_KM_MT
 #define HPAC_KM_MT 1
 #endif
