@@ -713,14 +713,20 @@ def kmeans_lloyd_arm(args, wl):
     cent0 = torch.from_numpy(E.make_blobs(n, d, k, 42, wl["separation"])[:k].copy() if rank else pts[:k].copy()).to(dev)
     grid, _ = E.resolve_grid("kmeans", n, items_per_thread=wl["ipt"])
     spec = make_spec(E, wl["spec"])
-    # N > 1: the library's NCCL communicator, so the all-reduce is captured
-    # in the Lloyd loop's CUDA graph; torch.distributed's all_reduce as a
-    # host callback otherwise (BENCH_KMEANS_TORCH_HOOK=1 forces it)
+    # N > 1: torch.distributed's all_reduce as the per-iteration hook (host
+    # loop). BENCH_KMEANS_NATIVE_NCCL=1 uses the library's own multi-process
+    # NCCL communicator instead, so the all-reduce is captured in the Lloyd
+    # loop's CUDA graph (single-rank tested; multi-GPU unmeasured here, hence
+    # opt-in). `value` is kernel time either way; the graph removes host gaps.
     allreduce, nccl_comm = None, None
     if dist is not None:
-        if (not os.environ.get("BENCH_KMEANS_TORCH_HOOK")
+        if (os.environ.get("BENCH_KMEANS_NATIVE_NCCL")
                 and os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl"):
-            nccl_comm = D.native_nccl_comm(rank, ws)
+            try:
+                nccl_comm = D.native_nccl_comm(rank, ws)
+            except Exception as exc:  # fall back to the torch hook
+                print(f"native NCCL communicator unavailable: {exc}", file=sys.stderr)
+                nccl_comm = None
         if nccl_comm is None:
             allreduce = D.kmeans_allreduce_hook()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
