@@ -367,8 +367,10 @@ struct AppKmeansDmma : AppKmeans {
 #endif
   // NT n-tiles starting at centroid j against MT m-tiles: x.c by DMMA, then
   // the (smallest, runner-up, argmin) update with this lane's 2 NT candidates
+  // (bj = this lane's fragment pointer for n-tile j/8, cj = &norm[j + 2t]:
+  // the loads below use constant offsets from them)
   template <int NT, int MT>
-  __device__ __forceinline__ static void dmma_tiles(const double2* bf, const double* cc, int j, int t,
+  __device__ __forceinline__ static void dmma_tiles(const double2* bj, const double* cj, int j, int t,
                                                     const double (&a)[MT][8], const double (&xx)[MT],
                                                     double (&m1)[MT], double (&m2)[MT], int (&best)[MT]) {
     double b[NT][8];
@@ -376,7 +378,7 @@ struct AppKmeansDmma : AppKmeans {
     for (int u = 0; u < NT; ++u)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double2 v = __ldg(bf + ((j / 8 + u) * 4 + q) * 32);
+        const double2 v = __ldg(bj + (u * 4 + q) * 32);
         b[u][2 * q] = v.x;
         b[u][2 * q + 1] = v.y;
       }
@@ -394,7 +396,7 @@ struct AppKmeansDmma : AppKmeans {
 #pragma unroll
     for (int u = 0; u < NT; ++u) {
       const int c0 = j + 8 * u + 2 * t;
-      const double n0 = __ldg(cc + c0), n1 = __ldg(cc + c0 + 1);
+      const double n0 = __ldg(cj + 8 * u), n1 = __ldg(cj + 8 * u + 1);
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         // non-finite data never passes: E in warp_eval is then inf/NaN
@@ -463,9 +465,11 @@ struct AppKmeansDmma : AppKmeans {
       // NT n-tiles (8 centroids each) per step: NT independent accumulation
       // chains per m-tile; a k % (8 NT) tail runs one n-tile at a time
       int j = 0;
-      for (; j + 8 * HPAC_KM_NT <= k; j += 8 * HPAC_KM_NT)
-        dmma_tiles<HPAC_KM_NT, MT>(bf, cc, j, t, a, xx, m1, m2, best);
-      for (; j < k; j += 8) dmma_tiles<1, MT>(bf, cc, j, t, a, xx, m1, m2, best);
+      const double2* bj = bf;
+      const double* cj = cc + 2 * t;
+      for (; j + 8 * HPAC_KM_NT <= k; j += 8 * HPAC_KM_NT, bj += 128 * HPAC_KM_NT, cj += 8 * HPAC_KM_NT)
+        dmma_tiles<HPAC_KM_NT, MT>(bj, cj, j, t, a, xx, m1, m2, best);
+      for (; j < k; j += 8, bj += 128, cj += 8) dmma_tiles<1, MT>(bj, cj, j, t, a, xx, m1, m2, best);
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         // merge the four lanes of the group (each saw 2 of every 8 centroids)
