@@ -185,3 +185,28 @@ def test_lloyd_run_to_run_deterministic(host_loop):
     assert torch.equal(a.centroids, b.centroids)
     for key in ("total_invocations", "approx_invocations", "divergent_warp_steps", "total_warp_steps"):
         assert a.stats[key] == b.stats[key], key
+
+
+@pytest.mark.parametrize("host_loop", [False, True])
+def test_lloyd_empty_cluster_keeps_centroid(host_loop):
+    """Duplicate initial centroids: ties go to the lower index, so the
+    duplicate's cluster starts empty and keeps its centroid (kmeans.hpp:142-143);
+    later it refills from running sums that restarted from zero."""
+    n, d, k = 8192, 32, 16
+    pts = E.make_blobs(n, d, k, 21, 10.0)
+    pts[3] = pts[1]  # Forgy init = first k points: centroid 3 duplicates centroid 1
+    grid, _ = E.resolve_grid("kmeans", n)
+    # iteration 1: cluster 3 is empty and keeps its centroid
+    r1 = E.kmeans_run(grid, dev(pts), k, None, max_iters=1, host_loop=host_loop)
+    assert not np.any(r1.assignments.cpu().numpy() == 3)
+    assert np.array_equal(r1.centroids.cpu().numpy()[3], pts[3])
+    # the full run (cluster 3 refills once centroid 1 moves: the running sums
+    # restart from zero) matches the oracle's full re-sums
+    r = E.kmeans_run(grid, dev(pts), k, None, max_iters=30, host_loop=host_loop)
+    a, c, it, conv, st = _oracle_kmeans(pts, k, grid, None, 30, 0)
+    assert r.iterations == it and r.converged == conv
+    ga = r.assignments.cpu().numpy()
+    mcr = float(np.mean(ga != a))
+    assert mcr <= 1e-3
+    if mcr == 0:
+        assert np.allclose(r.centroids.cpu().numpy(), c, rtol=1e-12, atol=1e-12)
