@@ -103,3 +103,15 @@ def test_dmma_equals_cuda_core_filter(case):
     want, _, _ = _run_oracle(pts, cents, grid, mp, None)
     assert np.array_equal(a, b), int(np.sum(a != b))
     assert np.array_equal(a, want)
+
+
+@pytest.mark.parametrize("n", [1, 5, 31, 33, 64 * 4 + 1])
+def test_dmma_tiny_and_ragged_n(n):
+    pts, _ = _blobs(max(n, 64), 32, 64, seed=n)
+    pts = pts[:n].copy()
+    cents = _blobs(64, 32, 64, seed=99)[1]
+    grid, mp = E.resolve_grid("kmeans", n, items_per_thread=4)
+    got, gst, gpaths = _run_gpu(pts, cents, grid, mp, None)
+    want, ost, opaths = _run_oracle(pts, cents, grid, mp, None)
+    assert np.array_equal(got, want)
+    assert gst["total_invocations"] == ost.total_invocations == n
