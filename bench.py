@@ -91,6 +91,26 @@ DMMA_PEAK_SOURCE = ("in-run FP64 tensor-op probe (hpac_probe_dmma_peak, mma.sync
                     "MEASURED_PEAKS.json has no FP64 figure")
 
 
+def lloyd_launches(r, dmma, random_first_exact):
+    """Kernels one hpac_kmeans_run launches (kmeans.cu): the label init; per
+    host-driven iteration the region (+ its DMMA operand kernel), the label
+    compaction, the update partials, their reduction, and - unless that
+    iteration converged - accumulate + recompute; in the CUDA graph, a state
+    init and per iteration those seven plus three timing/condition kernels
+    (accumulate/recompute always run there and return early on convergence)."""
+    region = 2 if dmma else 1
+    per_host = region + 3 + 2
+    it, host_its = r.iterations, r.iterations
+    n = 1
+    if r.graph:
+        host_its = 1 if random_first_exact else 0
+        n += 1 + (it - host_its) * (per_host + 3)
+    n += host_its * per_host
+    if r.converged and not r.graph:
+        n -= 2
+    return n
+
+
 def kmeans_uses_dmma(d, k):
     """The runtime's gate for AppKmeansDmma (runtime.cu prepare): 32 dims,
     k % 8 == 0, labels only, whole hardware warps (tpt 64)."""
@@ -884,9 +904,11 @@ def kmeans_lloyd_arm(args, wl):
         "quality": {"mcr": mcr}, "quality_ok": bool(mcr <= 0.01),
         "approx_rate": st["approx_invocations"] / max(1, st["total_invocations"]),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        # per iteration: region, update partials, partial reduction, centroid
-        # recompute (not after the converged one); + the label init per run
-        "gpu_launches": args.steps * (4 * it_a + 1 - (1 if r_a.converged else 0)), "clocks": clk,
+        "gpu_launches": args.steps * lloyd_launches(
+            r_a, kmeans_uses_dmma(d, k),
+            random_first_exact=spec is not None and spec.technique == abi.TECH_PERFO
+            and spec.perfo_kind == abi.PERFO_RANDOM),
+        "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
