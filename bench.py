@@ -702,7 +702,10 @@ def our_arm(args, wl):
         "approx_rate": st_apx["approx_invocations"] / max(1, st_apx["total_invocations"]),
         "divergent_fraction": st_apx["divergent_warp_steps"] / max(1, st_apx["total_warp_steps"]),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": args.steps, "clocks": clk, **extra_levels,
+        # one region kernel per step (+ the DMMA operand kernel for K-Means)
+        "gpu_launches": args.steps * (2 if wl["benchmark"] == "kmeans"
+                                      and kmeans_uses_dmma(wl["dims"], wl["k"]) else 1),
+        "clocks": clk, **extra_levels,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
