@@ -669,7 +669,7 @@ constexpr int kLatBmax = 33;  // register lattice up to N = 32*33 - 1 = 1055 ste
 constexpr int kBinoChunk = 256;
 constexpr int kBinoWarps = 2;  // = threads_per_team / 32 at the default tpt 64
 #ifndef HPAC_BINO_MIN_CTAS
-#define HPAC_BINO_MIN_CTAS 4
+#define HPAC_BINO_MIN_CTAS 8
 #endif
 
 // Decision codes in the chunk plan.
