@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define HPAC_ABI_VERSION 2
+#define HPAC_ABI_VERSION 3
 
 /* ---- status codes ------------------------------------------------------ */
 #define HPAC_OK 0
@@ -243,8 +243,10 @@ int hpac_stats_fetch(hpac_stats_t* stats);
    device buffer [k*dims sum changes | k count changes | 1 changed] (doubles;
    the iteration's moves: +x into a point's new cluster, -x out of its old
    one). Multi-GPU callers all-reduce it across ranks (e.g. ncclAllReduce /
-   torch all_reduce over NCCL); NULL = single device. */
-typedef void (*hpac_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
+   torch all_reduce over NCCL); NULL = single device. The hook returns 0 on
+   success; any other value aborts the run with HPAC_ERR_CUDA (a failed
+   all-reduce would otherwise leave each rank on its local partials). */
+typedef int (*hpac_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
 
 typedef struct hpac_kmeans_problem {
   int64_t n_points;     /* points in this shard */
@@ -286,9 +288,13 @@ int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_t* proble
 
 /* Native NCCL all-reduce usable as hpac_kmeans_problem_t.allreduce:
    `user` = the caller's ncclComm_t; sums the packed buffer in place on the
-   given stream. NCCL is loaded at run time (libnccl.so.2); 0 = unavailable. */
+   given stream. NCCL is loaded at run time (libnccl.so.2); 0 = unavailable.
+   hpac_nccl_allreduce returns HPAC_OK, HPAC_ERR_UNSUPPORTED (no NCCL / no
+   communicator) or HPAC_ERR_CUDA (ncclAllReduce failed);
+   hpac_nccl_check polls the communicator's asynchronous error state. */
 int hpac_nccl_available(void);
-void hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream);
+int hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream);
+int hpac_nccl_check(void* comm);
 /* Multi-process communicator for the hook (one process per GPU): rank 0
    writes a 128-byte NCCL unique id, the caller broadcasts it, every rank
    joins (ncclGetUniqueId / ncclCommInitRank). */

@@ -77,7 +77,7 @@ class Launch(C.Structure):
                 ("paths", C.c_void_p), ("synchronous", C.c_int32), ("reserved", C.c_int32)]
 
 
-ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 KMEANS_CENTROIDS_GIVEN = 8
 KMEANS_HOST_LOOP = 16
 
@@ -116,6 +116,8 @@ def _declare(lib):
         "hpac_mcr": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, P(C.c_double)]),
         "hpac_probe_fp64_peak": (C.c_int, [P(C.c_double)]),
         "hpac_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "hpac_nccl_allreduce": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+        "hpac_nccl_check": (C.c_int, [C.c_void_p]),
         "hpac_nccl_comm_init_rank": (C.c_int, [C.c_int, C.c_char_p, C.c_int, P(C.c_void_p)]),
         "hpac_probe_dmma_peak": (C.c_int, [P(C.c_double)]),
         "hpac_make_lavamd": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),

@@ -222,14 +222,23 @@ __global__ void kmeans_reduce_partials(const double* part, int nparts, int width
 }
 
 // Running sums and counts += this iteration's (all-reduced) changes; an
-// emptied cluster's sums restart from exact zero.
+// emptied cluster's sums restart from exact zero. One warp owns a cluster:
+// every lane reads the old count before lane 0 overwrites it, so no thread
+// can see a count another thread already updated (the sums and the count of
+// a cluster are never touched by two warps).
 __global__ void kmeans_accumulate(const double* red, int dims, int k, double* tot) {
   const int kd = k * dims;
   if (red[kd + k] == 0.0) return;  // converged: nothing moved
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kd + k; i += gridDim.x * blockDim.x) {
-    const int c = i < kd ? i / dims : i - kd;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < k; c += nwarps) {
     const double cnt = tot[kd + c] + red[kd + c];  // exact: integers below 2^53
-    tot[i] = i < kd ? (cnt > 0.0 ? tot[i] + red[i] : 0.0) : cnt;
+    for (int d = lane; d < dims; d += 32) {
+      const int i = c * dims + d;
+      tot[i] = cnt > 0.0 ? tot[i] + red[i] : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) tot[kd + c] = cnt;
   }
 }
 
@@ -455,12 +464,17 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
         pb->points, dist_label, list, oldlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
     kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, cs>>>(part, nparts,
                                                                               (int)(stride + 1), red);
-    if (pb->allreduce) pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, cs);
-    kmeans_accumulate<<<(int)((stride + 255) / 256), 256, 0, cs>>>(red, dims, k, tot);
+    int hook_rc = pb->allreduce ? pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, cs)
+                                : HPAC_OK;
+    kmeans_accumulate<<<(k + 7) / 8, 256, 0, cs>>>(red, dims, k, tot);
     kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, cs>>>(red, tot, dims, k, pb->centroids);
     loop_cond<<<1, 1, 0, cs>>>(ds, red + stride, left, pb->perfo_seed_base + (uint64_t)first + 1, h);
     cudaGraph_t body;
     cudaError_t ce = cudaStreamEndCapture(cs, &body);
+    if (hook_rc != HPAC_OK) {
+      cudaGetLastError();
+      return done(kfail(err, el, HPAC_ERR_CUDA, "kmeans all-reduce hook failed (status %d)", hook_rc));
+    }
     if (ge == cudaSuccess) ge = ce;
     if (ge == cudaSuccess) ge = cudaGetLastError();
     if (ge != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
@@ -471,6 +485,8 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
         (ge = cudaMemcpyAsync(&hs, ds, sizeof hs, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
         (ge = cudaStreamSynchronize(st)) != cudaSuccess)
       return done(kfail(err, el, HPAC_ERR_CUDA, "kmeans graph run: %s", cudaGetErrorString(ge)));
+    if (pb->allreduce == hpac_nccl_allreduce && hpac_nccl_check(pb->allreduce_user) != HPAC_OK)
+      return done(kfail(err, el, HPAC_ERR_CUDA, "kmeans all-reduce: NCCL communicator error"));
     res->iterations = first + hs.iter;
     res->converged = hs.converged;
     res->graph = 1;
@@ -541,7 +557,13 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
       rc = kfail(err, el, HPAC_ERR_CUDA, "kmeans update: %s", cudaGetErrorString(e));
       break;
     }
-    if (pb->allreduce) pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, st);
+    if (pb->allreduce) {
+      const int hrc = pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, st);
+      if (hrc != HPAC_OK) {
+        rc = kfail(err, el, HPAC_ERR_CUDA, "kmeans all-reduce hook failed (status %d)", hrc);
+        break;
+      }
+    }
     cudaMemcpyAsync(&h_changed, red + stride, sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaEventRecord(e1, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
@@ -555,7 +577,7 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
       res->converged = 1;
       break;
     }
-    kmeans_accumulate<<<(int)((stride + 255) / 256), 256, 0, st>>>(red, dims, k, tot);
+    kmeans_accumulate<<<(k + 7) / 8, 256, 0, st>>>(red, dims, k, tot);
     kmeans_recompute<<<(k * dims + 255) / 256, 256, 0, st>>>(red, tot, dims, k, pb->centroids);
   }
   res->stats.kernel_ms = res->region_ms + res->update_ms;

@@ -26,6 +26,7 @@ typedef int (*AllReduceFn)(const void*, void*, size_t, int /*dtype*/, int /*op*/
                            void* /*stream*/);
 typedef int (*InitAllFn)(void** /*comms*/, int, const int*);
 typedef int (*DestroyFn)(void*);
+typedef int (*AsyncErrFn)(void*, int*);
 struct NcclUid {  // nccl.h ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128)
   char internal[128];
 };
@@ -40,6 +41,7 @@ struct Nccl {
   DestroyFn destroy = nullptr;
   GetUidFn get_uid = nullptr;
   InitRankFn init_rank = nullptr;
+  AsyncErrFn async_err = nullptr;
 };
 
 Nccl* nccl() {
@@ -53,6 +55,7 @@ Nccl* nccl() {
     n.destroy = reinterpret_cast<DestroyFn>(dlsym(n.h, "ncclCommDestroy"));
     n.get_uid = reinterpret_cast<GetUidFn>(dlsym(n.h, "ncclGetUniqueId"));
     n.init_rank = reinterpret_cast<InitRankFn>(dlsym(n.h, "ncclCommInitRank"));
+    n.async_err = reinterpret_cast<AsyncErrFn>(dlsym(n.h, "ncclCommGetAsyncError"));
   });
   return n.all_reduce ? &n : nullptr;
 }
@@ -60,10 +63,27 @@ Nccl* nccl() {
 
 HPAC_API int hpac_nccl_available(void) { return nccl() != nullptr; }
 
-// hpac_allreduce_fn: `user` is the caller's ncclComm_t
-HPAC_API void hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream) {
+// hpac_allreduce_fn: `user` is the caller's ncclComm_t. A missing NCCL or
+// communicator and a failing ncclAllReduce are reported, never skipped: the
+// Lloyd loop then stops with HPAC_ERR_CUDA instead of continuing on this
+// rank's un-reduced partials.
+HPAC_API int hpac_nccl_allreduce(double* buf, int64_t count, void* user, void* stream) {
   Nccl* n = nccl();
-  if (n && user) n->all_reduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, user, stream);
+  if (!n || !user) return HPAC_ERR_UNSUPPORTED;
+  return n->all_reduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, user, stream) == 0
+             ? HPAC_OK
+             : HPAC_ERR_CUDA;
+}
+
+// Asynchronous communicator errors (ncclCommGetAsyncError): a collective
+// that failed after it was enqueued (e.g. inside a graph launch).
+HPAC_API int hpac_nccl_check(void* comm) {
+  Nccl* n = nccl();
+  if (!n || !comm) return HPAC_ERR_UNSUPPORTED;
+  if (!n->async_err) return HPAC_OK;
+  int state = 0;  // ncclSuccess
+  if (n->async_err(comm, &state) != 0) return HPAC_ERR_CUDA;
+  return state == 0 || state == 7 /* ncclInProgress */ ? HPAC_OK : HPAC_ERR_CUDA;
 }
 
 // Single-process communicators over `ndev` local devices (ncclCommInitAll),

@@ -54,14 +54,24 @@ int cuda_fail(char* err, size_t len, cudaError_t e, const char* where) {
   return fail(err, len, HPAC_ERR_CUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
 }
 
-// Per-host-thread launch scratch: device counters + pinned readback + events.
-struct Scratch {
-  int device = -1;
+// Per-host-thread launch scratch: a ring of slots, each with its own device
+// counters, pinned readback and events, so an asynchronous launch's counter
+// readback can never be overwritten by (or upload the counters of) the next
+// call; launches on different streams use different slots. A slot is reused
+// only after its previous readback completed (`done`).
+constexpr int kScratchSlots = 8;
+struct ScratchSlot {
   unsigned long long* d_cnt = nullptr;
   unsigned long long* h_cnt = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  hpac_stats_t last{};
-  bool pending = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, done = nullptr;
+  bool in_flight = false;  // readback enqueued, not yet waited for
+};
+struct Scratch {
+  int device = -1;
+  ScratchSlot slot[kScratchSlots];
+  int next = 0;
+  // the last asynchronous launch (hpac_stats_fetch)
+  int pending = -1;
   cudaStream_t pending_stream = nullptr;
   hpac_stats_t pending_base{};
 };
@@ -69,19 +79,55 @@ thread_local Scratch g_scratch;
 // set by the zero-copy host entry around its launch: generic per-thread engine
 thread_local bool g_force_thread_engine = false;
 
+void scratch_release() {
+  for (ScratchSlot& s : g_scratch.slot) {
+    if (s.done) cudaEventSynchronize(s.done);
+    if (s.d_cnt) cudaFree(s.d_cnt);
+    if (s.h_cnt) cudaFreeHost(s.h_cnt);
+    for (cudaEvent_t ev : {s.ev0, s.ev1, s.done})
+      if (ev) cudaEventDestroy(ev);
+    s = ScratchSlot{};
+  }
+  g_scratch.pending = -1;
+  g_scratch.device = -1;
+}
+
 cudaError_t scratch_ready() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (g_scratch.device == dev && g_scratch.d_cnt) return cudaSuccess;
-  if ((e = cudaMalloc(&g_scratch.d_cnt, sizeof(unsigned long long) * kNumCounters)) != cudaSuccess)
-    return e;
-  if ((e = cudaMallocHost(&g_scratch.h_cnt, sizeof(unsigned long long) * kNumCounters)) !=
-      cudaSuccess)
-    return e;
-  if ((e = cudaEventCreate(&g_scratch.ev0)) != cudaSuccess) return e;
-  if ((e = cudaEventCreate(&g_scratch.ev1)) != cudaSuccess) return e;
+  if (g_scratch.device == dev && g_scratch.slot[0].d_cnt) return cudaSuccess;
+  if (g_scratch.device >= 0) {  // the thread moved to another device
+    int cur = dev;
+    cudaSetDevice(g_scratch.device);
+    scratch_release();
+    cudaSetDevice(cur);
+  }
+  const size_t bytes = sizeof(unsigned long long) * kNumCounters;
+  for (ScratchSlot& s : g_scratch.slot) {
+    if ((e = cudaMalloc(&s.d_cnt, bytes)) != cudaSuccess) return e;
+    if ((e = cudaMallocHost(&s.h_cnt, bytes)) != cudaSuccess) return e;
+    if ((e = cudaEventCreate(&s.ev0)) != cudaSuccess) return e;
+    if ((e = cudaEventCreate(&s.ev1)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
   g_scratch.device = dev;
+  return cudaSuccess;
+}
+
+// Next free slot: waits for the slot's previous readback if it is still in
+// flight (only after kScratchSlots outstanding asynchronous launches).
+cudaError_t scratch_acquire(int* idx) {
+  const int i = g_scratch.next;
+  g_scratch.next = (i + 1) % kScratchSlots;
+  ScratchSlot& s = g_scratch.slot[i];
+  if (s.in_flight) {
+    cudaError_t e = cudaEventSynchronize(s.done);
+    if (e != cudaSuccess) return e;
+    s.in_flight = false;
+  }
+  if (g_scratch.pending == i) g_scratch.pending = -1;
+  *idx = i;
   return cudaSuccess;
 }
 
@@ -603,50 +649,56 @@ HPAC_API int hpac_run_region(const hpac_grid_t* grid, int64_t n, int32_t mapping
   bool sync = !launch || launch->synchronous;
   cudaError_t e = scratch_ready();
   if (e != cudaSuccess) return cuda_fail(err, el, e, "scratch");
+  int si = 0;
+  if ((e = scratch_acquire(&si)) != cudaSuccess) return cuda_fail(err, el, e, "scratch slot");
+  ScratchSlot& slot = g_scratch.slot[si];
   // counters: zero, barrier key = ~0
   unsigned long long init[kNumCounters];
   std::memset(init, 0, sizeof init);
   init[kCntBarrierKey] = ~0ull;
-  std::memcpy(g_scratch.h_cnt, init, sizeof init);
-  if ((e = cudaMemcpyAsync(g_scratch.d_cnt, g_scratch.h_cnt, sizeof init, cudaMemcpyHostToDevice,
-                           st)) != cudaSuccess)
+  std::memcpy(slot.h_cnt, init, sizeof init);
+  if ((e = cudaMemcpyAsync(slot.d_cnt, slot.h_cnt, sizeof init, cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
     return cuda_fail(err, el, e, "counter init");
-  pr.p.counters = g_scratch.d_cnt;
+  pr.p.counters = slot.d_cnt;
   // events bracket the kernel(s) only: the counter copies stay outside
-  cudaEventRecord(g_scratch.ev0, st);
+  if ((e = cudaEventRecord(slot.ev0, st)) != cudaSuccess) return cuda_fail(err, el, e, "event");
   if ((e = launch_prepared(pr, st)) != cudaSuccess) return cuda_fail(err, el, e, "kernel launch");
-  cudaEventRecord(g_scratch.ev1, st);
+  if ((e = cudaEventRecord(slot.ev1, st)) != cudaSuccess) return cuda_fail(err, el, e, "event");
+  e = cudaMemcpyAsync(slot.h_cnt, slot.d_cnt, sizeof init, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(err, el, e, "counter readback");
+  if ((e = cudaEventRecord(slot.done, st)) != cudaSuccess) return cuda_fail(err, el, e, "event");
+  slot.in_flight = true;
   if (!sync) {
-    // counters stay on device; hpac_stats_fetch reads them after the stream drains
-    g_scratch.pending = true;
+    // counters stay in this launch's slot; hpac_stats_fetch reads them
+    g_scratch.pending = si;
     g_scratch.pending_stream = st;
     g_scratch.pending_base = *stats;
-    e = cudaMemcpyAsync(g_scratch.h_cnt, g_scratch.d_cnt, sizeof init, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(err, el, e, "counter readback");
     return HPAC_OK;
   }
-  e = cudaMemcpyAsync(g_scratch.h_cnt, g_scratch.d_cnt, sizeof init, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return cuda_fail(err, el, e, "counter readback");
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(err, el, e, "kernel");
+  if ((e = cudaEventSynchronize(slot.done)) != cudaSuccess) return cuda_fail(err, el, e, "kernel");
+  slot.in_flight = false;
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, g_scratch.ev0, g_scratch.ev1);
-  counters_to_stats(g_scratch.h_cnt, stats);
+  cudaEventElapsedTime(&ms, slot.ev0, slot.ev1);
+  counters_to_stats(slot.h_cnt, stats);
   stats->kernel_ms = ms;
-  return finish_status(g_scratch.h_cnt, stats, pr.p.region.app, err, el);
+  return finish_status(slot.h_cnt, stats, pr.p.region.app, err, el);
 }
 
 HPAC_API int hpac_stats_fetch(hpac_stats_t* stats) {
-  if (!g_scratch.pending) return HPAC_ERR_CONFIG;
-  cudaError_t e = cudaStreamSynchronize(g_scratch.pending_stream);
+  if (g_scratch.pending < 0) return HPAC_ERR_CONFIG;
+  ScratchSlot& slot = g_scratch.slot[g_scratch.pending];
+  cudaError_t e = cudaEventSynchronize(slot.done);
   if (e != cudaSuccess) return HPAC_ERR_CUDA;
+  slot.in_flight = false;
   *stats = g_scratch.pending_base;
-  counters_to_stats(g_scratch.h_cnt, stats);
+  counters_to_stats(slot.h_cnt, stats);
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, g_scratch.ev0, g_scratch.ev1);
+  cudaEventElapsedTime(&ms, slot.ev0, slot.ev1);
   stats->kernel_ms = ms;
-  g_scratch.pending = false;
+  g_scratch.pending = -1;
   char buf[8];
-  return finish_status(g_scratch.h_cnt, stats, -1, buf, sizeof buf);
+  return finish_status(slot.h_cnt, stats, -1, buf, sizeof buf);
 }
 
 // Device-usable address of page-locked (pinned) host memory, else null.
@@ -722,16 +774,27 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
   cudaStream_t st = nullptr;
   cudaError_t e;
   std::vector<void*> bufs;
-  auto dalloc = [&](size_t bytes, const void* src, bool copy) -> void* {
-    if (!bytes) return nullptr;
+  cudaError_t alloc_e = cudaSuccess;  // first allocation / copy failure
+  const char* alloc_what = nullptr;
+  auto dalloc = [&](size_t bytes, const void* src, bool copy, const char* what) -> void* {
+    if (!bytes || alloc_e != cudaSuccess) return nullptr;
     void* d = nullptr;
     cudaMemPool_t pool = host_entry_pool();
-    if ((pool ? cudaMallocFromPoolAsync(&d, bytes, pool, st) : cudaMallocAsync(&d, bytes, st)) !=
-        cudaSuccess)
+    cudaError_t ae = pool ? cudaMallocFromPoolAsync(&d, bytes, pool, st) : cudaMallocAsync(&d, bytes, st);
+    if (ae == cudaSuccess) {
+      bufs.push_back(d);
+      if (copy && src) ae = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
+    }
+    if (ae != cudaSuccess) {
+      alloc_e = ae;
+      alloc_what = what;
       return nullptr;
-    bufs.push_back(d);
-    if (copy && src) cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
+    }
     return d;
+  };
+  auto release = [&]() {
+    for (void* b : bufs) cudaFreeAsync(b, st);
+    cudaStreamSynchronize(st);
   };
   hpac_region_t d = r;
   // Zero-copy for the stream-once regions (Blackscholes; the K-Means labels
@@ -750,15 +813,21 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
     d.in = (const double*)pinned_device_ptr(r.in);
     d.out = (double*)pinned_device_ptr(r.out);
     d.labels = (int32_t*)pinned_device_ptr(r.labels);
-    d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true);  // read per CTA: stage
+    d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true, "centroids");  // read per CTA: stage
   } else {
-    d.in = (const double*)dalloc(in_bytes, r.in, true);
-    d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true);
-    d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true);
+    d.in = (const double*)dalloc(in_bytes, r.in, true, "inputs");
+    d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true, "table_out");
+    d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true, "encounters");
     // outputs start from the caller's contents (skipped items keep them)
-    d.out = (double*)dalloc(out_bytes, r.out, true);
-    d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true);
-    d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true);
+    d.out = (double*)dalloc(out_bytes, r.out, true, "outputs");
+    d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true, "centroids");
+    d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true, "labels");
+  }
+  if (alloc_e != cudaSuccess) {
+    release();
+    cudaGetLastError();
+    return fail(err, el, HPAC_ERR_CUDA, "CUDA error staging %s: %s", alloc_what,
+                cudaGetErrorString(alloc_e));
   }
   hpac_launch_t L{};
   L.stream = st;
@@ -768,8 +837,13 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
   g_force_thread_engine = false;
   if (stats) stats->zero_copy = zero_copy ? 1 : 0;
   if (rc == HPAC_OK && !zero_copy) {
-    if (out_bytes) cudaMemcpyAsync(r.out, d.out, out_bytes, cudaMemcpyDeviceToHost, st);
-    if (lab_bytes) cudaMemcpyAsync(r.labels, d.labels, lab_bytes, cudaMemcpyDeviceToHost, st);
+    if (out_bytes && (e = cudaMemcpyAsync(r.out, d.out, out_bytes, cudaMemcpyDeviceToHost, st)) !=
+                         cudaSuccess)
+      rc = cuda_fail(err, el, e, "copying outputs to the host");
+    if (rc == HPAC_OK && lab_bytes &&
+        (e = cudaMemcpyAsync(r.labels, d.labels, lab_bytes, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess)
+      rc = cuda_fail(err, el, e, "copying labels to the host");
   }
   for (void* b : bufs) cudaFreeAsync(b, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess && rc == HPAC_OK)

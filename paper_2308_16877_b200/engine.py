@@ -383,12 +383,24 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
     pb.perfo_seed_base = perfo_seed_base
     pb.reduce_buf = _ptr(red)
     cb = None
+    hook_error = []
     if nccl_comm is not None:
         pb.allreduce = C.cast(abi.lib().hpac_nccl_allreduce, abi.ALLREDUCE_FN)
         pb.allreduce_user = nccl_comm
     elif allreduce is not None:
         def _cb(buf, count, user, st):
-            allreduce(red)
+            # The library produced `red` on stream `st` and reads it back there:
+            # run the collective on that same stream (torch orders NCCL against
+            # its current stream). An exception cannot cross the C boundary, so
+            # it is kept, reported as a nonzero status (the loop stops with
+            # HPAC_ERR_CUDA) and re-raised below.
+            try:
+                with torch.cuda.stream(torch.cuda.ExternalStream(st or 0, device=points.device)):
+                    allreduce(red)
+                return 0
+            except BaseException as exc:  # noqa: BLE001 - re-raised after the run
+                hook_error.append(exc)
+                return 1
         cb = abi.ALLREDUCE_FN(_cb)
         pb.allreduce = cb
     res = abi.KmeansResult()
@@ -397,6 +409,8 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
     rc = abi.lib().hpac_kmeans_run(C.byref(grid.c()), C.byref(pb),
                                    C.byref(spec) if spec is not None else None, st,
                                    C.byref(res), err, 1024)
+    if hook_error:
+        raise CudaError(f"kmeans all-reduce hook failed: {hook_error[0]!r}") from hook_error[0]
     if rc:
         _raise(rc, err, res.stats)
     return KmeansResult(assign, cent, res.iterations, bool(res.converged), res.stats.as_dict(),

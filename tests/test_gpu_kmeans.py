@@ -210,3 +210,73 @@ def test_lloyd_empty_cluster_keeps_centroid(host_loop):
     assert mcr <= 1e-3
     if mcr == 0:
         assert np.allclose(r.centroids.cpu().numpy(), c, rtol=1e-12, atol=1e-12)
+
+
+def test_failing_python_hook_raises():
+    """A Python all-reduce hook that raises must stop the Lloyd loop with an
+    error (the exception cannot cross the C boundary; it is re-raised), not
+    continue on this rank's un-reduced partials."""
+    pts = E.make_blobs(2048, 4, 8, 5, 8.0)
+    grid, _ = E.resolve_grid("kmeans", 2048)
+
+    def broken(buf):
+        raise RuntimeError("peer lost")
+
+    with pytest.raises(E.CudaError, match="peer lost"):
+        E.kmeans_run(grid, dev(pts), 8, allreduce=broken)
+
+
+def test_hook_nonzero_status_is_an_error():
+    """hpac_allreduce_fn returning nonzero -> HPAC_ERR_CUDA from hpac_kmeans_run
+    (host loop and graph capture alike), with the failing status in the message."""
+    pts = dev(E.make_blobs(2048, 4, 8, 5, 8.0))
+    n, d, k = 2048, 4, 8
+    grid, _ = E.resolve_grid("kmeans", n)
+    calls = []
+
+    @abi.ALLREDUCE_FN
+    def failing(buf, count, user, st):
+        calls.append(count)
+        return 7
+
+    for flags in (0, abi.KMEANS_HOST_LOOP):
+        cent = torch.empty((k, d), dtype=torch.float64, device="cuda")
+        assign = torch.empty(n, dtype=torch.int32, device="cuda")
+        pb = abi.KmeansProblem()
+        pb.n_points, pb.dims, pb.k = n, d, k
+        pb.points, pb.centroids, pb.assignments = pts.data_ptr(), cent.data_ptr(), assign.data_ptr()
+        pb.max_iters, pb.flags = 10, flags
+        pb.allreduce = failing
+        res = abi.KmeansResult()
+        err = C.create_string_buffer(512)
+        rc = abi.lib().hpac_kmeans_run(C.byref(grid.c()), C.byref(pb), None, None, C.byref(res), err, 512)
+        assert rc == abi.ERR_CUDA, (rc, err.value)
+        assert b"status 7" in err.value
+    assert calls and all(c == k * d + k + 1 for c in calls)
+
+
+def test_nccl_hook_without_communicator_is_an_error():
+    rc = abi.lib().hpac_nccl_allreduce(None, 0, None, None)
+    assert rc in (abi.ERR_UNSUPPORTED,)
+
+
+def test_lloyd_cluster_losing_half_its_points():
+    """Regression for the running-sum update (kmeans_accumulate): with k*d + k
+    > 256 the update spans several CTAs, and a cluster that loses at least half
+    of its points in one iteration must keep correct sums (it did not when a
+    sum thread could read the already-updated count). Forgy init on a
+    adversarial point order: the first k points all sit in one blob, so the
+    first iterations move most points between clusters."""
+    n, d, k = 8192, 32, 64
+    pts = E.make_blobs(n, d, k, 11, 30.0)
+    order = np.argsort(np.arange(n) % k, kind="stable")  # blob 0's points first
+    pts = np.ascontiguousarray(pts[order])
+    grid, _ = E.resolve_grid("kmeans", n)
+    want_a, want_c, want_it, want_conv, _ = _oracle_kmeans(pts, k, grid, None, 40)
+    for host_loop in (False, True):
+        for _ in range(3):
+            r = E.kmeans_run(grid, dev(pts), k, max_iters=40, host_loop=host_loop)
+            assert r.iterations == want_it and r.converged == want_conv
+            mcr = float((r.assignments.cpu().numpy() != want_a).mean())
+            assert mcr <= 1e-3, mcr
+            assert np.allclose(r.centroids.cpu().numpy(), want_c, rtol=1e-9, atol=1e-9)
