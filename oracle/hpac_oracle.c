@@ -130,6 +130,30 @@ ORACLE_API int oracle_binomial_price(const double* o, int n_steps, int american,
   return 0;
 }
 
+/* Whole portfolios (test convenience; options are independent). */
+ORACLE_API int oracle_bs_prices(const double* opts, int64_t n, double* out) {
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+  for (int64_t i = 0; i < n; ++i)
+    if (oracle_black_scholes_call(opts + (size_t)i * 5, out + i)) {
+      out[i] = NAN;
+      ++bad;
+    }
+  return bad;
+}
+
+ORACLE_API int oracle_binomial_prices(const double* opts, int64_t n, int n_steps, int american,
+                                      int is_put, double* out) {
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : bad)
+  for (int64_t i = 0; i < n; ++i)
+    if (oracle_binomial_price(opts + (size_t)i * 5, n_steps, american, is_put, out + i)) {
+      out[i] = NAN;
+      ++bad;
+    }
+  return bad;
+}
+
 /* ------------------------------------------------------------------ */
 /* TAF, taf.hpp:29-163                                                 */
 /* ------------------------------------------------------------------ */
@@ -493,6 +517,10 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
     case HPAC_APP_KMEANS: {
       /* bench/kmeans.hpp:85-95 */
       int dims = r->kmeans_dims, k = r->kmeans_k;
+      if (r->table_out) { /* distances precomputed by kmeans_distances (same arithmetic) */
+        for (int c = 0; c < k; ++c) out[c] = r->table_out[(size_t)idx * k + c];
+        return 0;
+      }
       const double* pt = r->in + (size_t)idx * dims;
       for (int c = 0; c < k; ++c) {
         double ssq = 0.0;
@@ -678,9 +706,32 @@ typedef struct {
   int64_t idx;
 } lane_work;
 
+/* Teams [team_begin, team_end) of the logical grid only (0, 0 = all): every
+   thread keeps its global id and stride, so the executed teams make exactly
+   the decisions they make in the whole-grid run (each team's technique state
+   is its own); the C-ABI's hpac_launch_t.team_begin/team_end counterpart. */
+static int run_region_range(const hpac_grid_t* g, int64_t n, int32_t mapping,
+                            const hpac_region_t* reg, const hpac_spec_t* spec, hpac_stats_t* st,
+                            uint8_t* paths, int32_t team_begin, int32_t team_end, char* err,
+                            size_t el);
+
 ORACLE_API int oracle_run_region(const hpac_grid_t* g, int64_t n, int32_t mapping,
                                  const hpac_region_t* reg, const hpac_spec_t* spec,
                                  hpac_stats_t* st, uint8_t* paths, char* err, size_t el) {
+  return run_region_range(g, n, mapping, reg, spec, st, paths, 0, 0, err, el);
+}
+
+ORACLE_API int oracle_run_region_teams(const hpac_grid_t* g, int64_t n, int32_t mapping,
+                                       const hpac_region_t* reg, const hpac_spec_t* spec,
+                                       hpac_stats_t* st, uint8_t* paths, int32_t team_begin,
+                                       int32_t team_end, char* err, size_t el) {
+  return run_region_range(g, n, mapping, reg, spec, st, paths, team_begin, team_end, err, el);
+}
+
+static int run_region_range(const hpac_grid_t* g, int64_t n, int32_t mapping,
+                            const hpac_region_t* reg, const hpac_spec_t* spec, hpac_stats_t* st,
+                            uint8_t* paths, int32_t team_begin, int32_t team_end, char* err,
+                            size_t el) {
   int rc;
   memset(st, 0, sizeof *st);
   if (err && el) err[0] = 0;
@@ -788,8 +839,14 @@ ORACLE_API int oracle_run_region(const hpac_grid_t* g, int64_t n, int32_t mappin
   uint8_t* lpath = (uint8_t*)malloc((size_t)ws); /* 0 inactive, 1 accurate, 2 approx */
   rc = 0;
 
+  const int tb = (team_begin || team_end) ? team_begin : 0;
+  const int te = (team_begin || team_end) ? team_end : nteams;
+  if (tb < 0 || te > nteams || tb > te) {
+    rc = fail(err, el, HPAC_ERR_CONFIG, "team range [%d, %d) outside the grid's %d teams", tb, te,
+              nteams);
+  }
   for (int64_t step = 0; step < steps && !rc; ++step) {
-    for (int team = 0; team < nteams && !rc; ++team) {
+    for (int team = tb; team < te && !rc; ++team) {
       int rounds = 0;
       for (int local = 0; local < tpt; ++local) {
         int tid = team * tpt + local;
@@ -990,6 +1047,26 @@ ORACLE_API int oracle_run_region(const hpac_grid_t* g, int64_t n, int32_t mappin
 /* ------------------------------------------------------------------ */
 /* K-Means Lloyd loop, bench/kmeans.hpp:62-144                         */
 /* ------------------------------------------------------------------ */
+/* All n*k distances of one iteration, the region's evaluate arithmetic
+   (bench/kmeans.hpp:85-95: no-FMA sum in dimension order, IEEE sqrt) per
+   point; points are independent, so the threads only change the speed. The
+   engine then reads them instead of recomputing each evaluated point. */
+static void kmeans_distances(const double* points, int64_t n, int dims, int k, const double* cent,
+                             double* dcache) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double* pt = points + (size_t)i * dims;
+    for (int c = 0; c < k; ++c) {
+      double ssq = 0.0;
+      for (int d = 0; d < dims; ++d) {
+        double diff = pt[d] - cent[c * dims + d];
+        ssq += diff * diff;
+      }
+      dcache[(size_t)i * k + c] = sqrt(ssq);
+    }
+  }
+}
+
 ORACLE_API int oracle_kmeans_benchmark(const double* points, int64_t n, int dims, int k,
                                        const hpac_grid_t* g, const hpac_spec_t* spec,
                                        int max_iters, uint64_t perfo_seed_base,
@@ -998,6 +1075,7 @@ ORACLE_API int oracle_kmeans_benchmark(const double* points, int64_t n, int dims
                                        hpac_stats_t* total, char* err, size_t el) {
   double* cent = (double*)malloc(sizeof(double) * (size_t)k * dims);
   double* dist = (double*)calloc((size_t)n * k, sizeof(double));
+  double* dcache = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1) * k);
   int32_t* next = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
   double* sums = (double*)malloc(sizeof(double) * (size_t)k * dims);
   int64_t* counts = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
@@ -1019,6 +1097,7 @@ ORACLE_API int oracle_kmeans_benchmark(const double* points, int64_t n, int dims
   r.in = points;
   r.centroids = cent;
   r.out = dist;
+  r.table_out = dcache;
   r.labels = NULL;
   hpac_spec_t sp;
   if (spec) sp = *spec;
@@ -1030,6 +1109,7 @@ ORACLE_API int oracle_kmeans_benchmark(const double* points, int64_t n, int dims
        have a stale label to keep; the reference modes keep label 0) */
     const int exact_iter = spec && spec->technique == HPAC_TECH_PERFO &&
                            spec->perfo_kind == HPAC_PERFO_RANDOM && iter == 1;
+    kmeans_distances(points, n, dims, k, cent, dcache);
     rc = oracle_run_region(g, n, HPAC_MAP_PER_THREAD, &r, (spec && !exact_iter) ? &sp : NULL, &st,
                            NULL, err, el);
     if (rc) break;
@@ -1070,6 +1150,7 @@ ORACLE_API int oracle_kmeans_benchmark(const double* points, int64_t n, int dims
   if (centroids_out) memcpy(centroids_out, cent, sizeof(double) * (size_t)k * dims);
   free(cent);
   free(dist);
+  free(dcache);
   free(next);
   free(sums);
   free(counts);

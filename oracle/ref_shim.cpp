@@ -330,6 +330,52 @@ REF_API int ref_binomial_price(const double* o, int n_steps, int american, int i
   }
 }
 
+// ---- the reference's stock benchmark regions and plain loops ---------------
+// bench.py's reference arm times these: bench::binomial_region /
+// bench::blackscholes_region (bench/binomial.hpp:74-94,
+// bench/blackscholes.hpp:72-92) through run_region exactly as
+// bench::detail::run_benchmark builds them (bench/run.hpp:133-165), and the
+// plain per-option loops binomial_reference / blackscholes_reference
+// (bench/binomial.hpp:96-102, bench/blackscholes.hpp:94-98).
+static std::vector<bench::BsOption> to_options(const double* o, int64_t n) {
+  std::vector<bench::BsOption> v(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i)
+    v[i] = bench::BsOption{o[5 * i], o[5 * i + 1], o[5 * i + 2], o[5 * i + 3], o[5 * i + 4]};
+  return v;
+}
+
+REF_API int ref_bench_binomial_run(const double* opts, int64_t n, int n_steps,
+                                   const hpac_grid_t* g, const hpac_spec_t* s, double* prices,
+                                   hpac_stats_t* st, char* err, size_t errlen) {
+  const std::vector<bench::BsOption> options = to_options(opts, n);
+  std::vector<double> out(static_cast<size_t>(n), 0.0);
+  Region region = bench::binomial_region(options, n_steps, out);
+  int rc = run_guarded(g, n, HPAC_MAP_PER_TEAM, region, s, st, err, errlen);
+  if (prices) std::memcpy(prices, out.data(), sizeof(double) * static_cast<size_t>(n));
+  return rc;
+}
+
+REF_API int ref_bench_blackscholes_run(const double* opts, int64_t n, const hpac_grid_t* g,
+                                       const hpac_spec_t* s, double* prices, hpac_stats_t* st,
+                                       char* err, size_t errlen) {
+  const std::vector<bench::BsOption> options = to_options(opts, n);
+  std::vector<double> out(static_cast<size_t>(n), 0.0);
+  Region region = bench::blackscholes_region(options, out);
+  int rc = run_guarded(g, n, HPAC_MAP_PER_THREAD, region, s, st, err, errlen);
+  if (prices) std::memcpy(prices, out.data(), sizeof(double) * static_cast<size_t>(n));
+  return rc;
+}
+
+REF_API void ref_binomial_reference(const double* opts, int64_t n, int n_steps, double* prices) {
+  std::vector<double> out = bench::binomial_reference(to_options(opts, n), n_steps);
+  std::memcpy(prices, out.data(), sizeof(double) * static_cast<size_t>(n));
+}
+
+REF_API void ref_blackscholes_reference(const double* opts, int64_t n, double* prices) {
+  std::vector<double> out = bench::blackscholes_reference(to_options(opts, n));
+  std::memcpy(prices, out.data(), sizeof(double) * static_cast<size_t>(n));
+}
+
 REF_API double ref_synthetic_value(int profile, int64_t i, uint64_t seed) {
   return bench::synthetic_value(static_cast<bench::SyntheticProfile>(profile), i, seed);
 }
