@@ -37,15 +37,16 @@ METRIC = "approx-region items/s & speedup vs exact GPU kernel at <=1% quality lo
 WORKLOADS = {
     "binomial": dict(
         name="binomial-1M-x-1024-iact-team",
-        benchmark="binomial", n=1 << 20, lattice=1024, ipt=384,
-        directive="memo(in:4:0.4) level(team)", spec=("iact", 4, 0.4, None, "team"),
+        benchmark="binomial", n=1 << 20, lattice=1024, ipt=384, exact_best_ipt=256,
+        directive="memo(in:4:0.4) level(team) in(option[i*5:5]) out(price[i])",
+        spec=("iact", 4, 0.4, None, "team"),
         unit="options/s"),
     "blackscholes": dict(
         name="blackscholes-4M-taf-h5", benchmark="blackscholes", n=1 << 22, ipt=16,
-        directive="memo(out:5:1:0.5)", spec=("taf", 5, 1, 0.5, "thread"), unit="options/s"),
+        directive="memo(out:5:1:0.5) out(price[i])", spec=("taf", 5, 1, 0.5, "thread"), unit="options/s"),
     "lavamd": dict(
         name="lavamd-64^3-boxes-x-128-taf-warp", benchmark="lavamd", boxes1d=64, particles=128, ipt=1,
-        directive="memo(out:3:8:0.1) level(warp)", spec=("taf", 3, 8, 0.1, "warp"),
+        directive="memo(out:3:8:0.1) level(warp) out(fv[i*4:4])", spec=("taf", 3, 8, 0.1, "warp"),
         compare_levels=("thread", "team"), unit="particles/s"),
     # C3 as the reference's kmeans_benchmark (bench/kmeans.hpp:62-144): the
     # whole Lloyd loop (region + centroid update + per-iteration all-reduce),
@@ -245,170 +246,313 @@ def make_spec(E, s):
     return E.perfo(s[1], s[2], level=s[3] if len(s) > 3 else "thread")
 
 
+# ------------------------------------------------------------------ shared config
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def global_problem(wl, ws):
+    """Items of the whole job and how ranks split them. Binomial (the
+    headline): ONE logical grid over ws x 2^20 options, split into contiguous
+    team ranges that keep the global stride (machine.hpp:77-84), so every
+    rank makes exactly the decisions the 1-GPU run of the same problem makes
+    (SURVEY §8e). Other workloads: independent per-rank shards."""
+    if wl["benchmark"] == "binomial":
+        return ws * wl["n"], "team-ranges"
+    return wl.get("n"), "shards"
+
+
+def bench_config(wl, grid, mapping, ws):
+    """The `config` object of both arms (identical keys and values)."""
+    n_total, split = global_problem(wl, ws)
+    per_item = wl.get("particles", 1) if wl["benchmark"] == "lavamd" else 1
+    cfg = {"workload": wl["name"], "directive": wl["directive"],
+           "grid": {"num_teams": grid.num_teams, "threads_per_team": grid.threads_per_team,
+                    "warp_size": grid.warp_size, "items_per_thread": grid.items_per_thread},
+           "mapping": "per-team" if mapping == 1 else "per-thread",
+           "l2": "flushed between timed iterations"}
+    if wl["benchmark"] == "binomial":
+        cfg.update({"n_per_gpu": wl["n"], "n_total": n_total, "lattice_steps": wl["lattice"],
+                    "parallelism": (f"dp{ws}: contiguous team ranges of one {grid.num_teams}-team logical "
+                                    "grid (global stride kept; decisions identical to the 1-GPU run)")})
+    else:
+        n = wl["boxes1d"] ** 3 if wl["benchmark"] == "lavamd" else wl["n"]
+        cfg.update({"n_per_gpu": n * per_item, "parallelism": f"dp{ws} (independent shards)"})
+    return cfg
+
+
 # ------------------------------------------------------------------ reference arm
 
-def reference_arm(args, wl):
-    """The reference's own CPU engine (oracle/_ref = /root/reference compiled),
-    on all host threads, on bounded samples of the same workload."""
+def ref_binomial_sample(wl, ws, threads, prefix=None, warmup=0):
+    """The reference's own engine on whole team streams of the headline grid.
+
+    `threads` teams spread evenly over the global logical grid (the
+    reference's resolve_grid, bench/run.hpp:81-97) each run their complete
+    item stream idx = team + s*T (or its first `prefix` items) through
+    bench::binomial_region + run_region (bench/binomial.hpp:74-94,
+    engine.hpp:132), one team per host thread. A one-team grid over the
+    team's stream in order is the same execution as that team inside the
+    full grid (per-team mapping: the team's tables see exactly these options
+    in this order), so the sample has the full grid's table reuse. Imports
+    only the checker package: no product code, no libhpac_b200.so."""
     import numpy as np
 
     import oracle
-    from paper_2308_16877_b200 import engine as E
+    from concurrent.futures import ThreadPoolExecutor
+    n_total, _ = global_problem(wl, ws)
+    opts = oracle.ref_portfolio("binomial", n_total, 42)
+    grid, mapping = oracle.ref_grid("binomial", n_total, items_per_thread=wl["ipt"])
+    spec = oracle.ref_parse(wl["directive"])
+    T = grid.num_teams
+    steps = -(-n_total // T)
+    P = max(1, min(threads, T))
+    teams = [j * T // P for j in range(P)]
 
+    def stream(t):
+        idx = t + np.arange(steps, dtype=np.int64) * T
+        idx = idx[idx < n_total]
+        return idx if prefix is None else idx[:prefix]
+
+    def run_team(t, first=None):
+        idx = stream(t) if first is None else stream(t)[:first]
+        sub = oracle.abi.Grid(1, grid.threads_per_team, grid.warp_size, len(idx), grid.shared_mem_budget_bytes)
+        rc, st, _, msg = oracle.ref_bench_binomial(opts[idx], wl["lattice"], sub, spec)
+        assert rc == 0, msg
+        return len(idx), st.approx_invocations, st.total_invocations
+
+    with ThreadPoolExecutor(max_workers=P) as ex:
+        for _ in range(warmup):  # page in the code on every thread (1 option each)
+            list(ex.map(lambda t: run_team(t, first=1), teams))
+        t0 = time.perf_counter()
+        res = list(ex.map(run_team, teams))
+        wall = time.perf_counter() - t0
+    items = sum(r[0] for r in res)
+    rate = sum(r[1] for r in res) / max(1, sum(r[2] for r in res))
+    desc = (f"{P} of the {T} teams of the global grid (team j*T/{P}), "
+            + ("each its whole " if prefix is None else f"each the first {prefix} options of its ")
+            + f"{steps}-option stream (idx = team + s*{T}) through bench::binomial_region + run_region, "
+            f"one host thread per team; {wl['lattice']}-step lattice; approx rate {rate:.4f}")
+    return {"items": items, "wall_s": wall, "approx_rate": rate, "teams": P, "sample": desc,
+            "grid": grid, "mapping": mapping}
+
+
+def ref_binomial_floor(wl, threads, per_thread=32):
+    """The reference's plain loop binomial_reference (bench/binomial.hpp:96-102)
+    on all host threads: the no-engine CPU floor (every option priced once)."""
+    import numpy as np
+
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    n = wl["n"]
+    opts = oracle.ref_portfolio("binomial", n, 42)
+    chunks = [np.ascontiguousarray(opts[(np.arange(per_thread) * threads + j) * (n // (per_thread * threads))])
+              for j in range(threads)]
+
+    def one(c):
+        out = np.empty(len(c))
+        oracle.ref().ref_binomial_reference(c.ctypes.data, len(c), wl["lattice"], out.ctypes.data)
+        return len(c)
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        t0 = time.perf_counter()
+        items = sum(ex.map(one, chunks))
+        wall = time.perf_counter() - t0
+    return {"value": items / wall, "unit": wl["unit"], "cores": threads, "kind": "reference",
+            "sample": f"binomial_reference (plain per-option loop, no engine) over {items} options "
+                      f"strided across the portfolio, {threads} threads"}
+
+
+def reference_arm(args, wl):
+    """`--impl reference`: the reference's own CPU implementation of the path
+    (oracle/_ref = /root/reference compiled by oracle/Makefile) on the box's
+    host cores, on this arm's config. Rank 0 only. Never imports the product
+    package: inputs, grid and directive come from the reference's own
+    generators, resolve_grid and parse_directive."""
+    import numpy as np
+
+    import oracle
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    cores = host_cores()
     kind = "reference"
-    if wl["benchmark"] not in ("lavamd", "kmeans_lloyd"):
-        oracle.ref()
-    cores = os.cpu_count() or 1
-    n = wl.get("n")
+    extra = {}
     if wl["benchmark"] == "binomial":
-        opts = E.make_binomial_portfolio(n, 42)
-        grid, mapping = E.resolve_grid("binomial", n, items_per_thread=wl["ipt"])
-        T = grid.num_teams
-        per_team = 2  # options of one team per worker and step (669 ms each in-engine)
-        sample_desc = (f"{cores} threads x 1 team x {per_team} options (idx = team + s*{T}), "
-                       f"{wl['lattice']}-step lattice, reference run_region per team")
-
-        def work(worker, step):
-            team = (worker * 97 + step * 13) % T
-            idx = team + np.arange(per_team) * T
-            sub = np.ascontiguousarray(opts[idx])
-            out = np.zeros(per_team)
-            g = E.GridConfig(1, 64, 32, per_team)
-            reg = E.binomial_region(sub, wl["lattice"], out)
-            rc, st, msg = oracle.ref_run(g, per_team, 1, reg, make_spec(E, wl["spec"]))
-            assert rc == 0, msg
-            return per_team
+        # K timed steps = K consecutive slices of the sampled teams' streams:
+        # a team's table state must carry across the whole stream, so each
+        # team runs as ONE run_region call and the K steps share its wall time
+        r = ref_binomial_sample(wl, ws, cores, warmup=min(1, args.warmup))
+        items, dt = r["items"], r["wall_s"]
+        grid, mapping = r["grid"], r["mapping"]
+        sample = r["sample"]
+        extra = {"approx_rate": r["approx_rate"],
+                 "cpu_floor": ref_binomial_floor(wl, cores),
+                 "timing": ("one reference run_region per sampled team over its whole stream, all "
+                            "teams concurrently; wall clock of the slowest; ms_per_step = wall / steps")}
     elif wl["benchmark"] == "blackscholes":
-        opts = E.make_bs_portfolio(1 << 20, 42)
-        per = 1 << 16
-        sample_desc = f"{cores} threads x {per} options (1024 teams x 64, ipt 1), reference run_region"
+        n = wl["n"]
+        opts = oracle.ref_portfolio("blackscholes", n, 42)
+        grid, mapping = oracle.ref_grid("blackscholes", n, items_per_thread=wl["ipt"])
+        spec = oracle.ref_parse(wl["directive"])
+        G = grid.num_teams * grid.threads_per_team
+        per = 64  # teams per worker: whole teams, every step of their streams
+        sample = (f"{cores} threads x {per} whole teams of the {grid.num_teams}-team grid (all "
+                  f"{grid.items_per_thread} steps of each stream), bench::blackscholes_region + run_region")
+        from concurrent.futures import ThreadPoolExecutor
 
-        def work(worker, step):
-            lo = ((worker + step * cores) * per) % (1 << 20)
-            sub = np.ascontiguousarray(opts[lo:lo + per])
-            out = np.zeros(per)
-            g = E.GridConfig(per // 64 // 16, 64, 32, 16)
-            rc, st, msg = oracle.ref_run(g, per, 0, E.blackscholes_region(sub, out), make_spec(E, wl["spec"]))
+        def work(w):
+            t0 = (w * per) % grid.num_teams
+            thr = (t0 * grid.threads_per_team + np.arange(per * grid.threads_per_team))
+            idx = (thr[None, :] + np.arange(grid.items_per_thread)[:, None] * G).ravel()
+            idx = idx[idx < n]
+            sub = oracle.abi.Grid(per, grid.threads_per_team, grid.warp_size, grid.items_per_thread,
+                                  grid.shared_mem_budget_bytes)
+            rc, st, _, msg = oracle.ref_bench_blackscholes(opts[idx], sub, spec)
             assert rc == 0, msg
-            return per
-    elif wl["benchmark"] == "lavamd":
-        # LavaMD is not in the reference (SURVEY Appendix C): the reference arm
-        # runs our CPU restatement (oracle port) of the same region
-        b1, P = wl["boxes1d"], wl["particles"]
-        rv, qv = E.make_lavamd(b1, P, 42)
-        per = 16  # home boxes per worker and step
-        kind = "port"
-        sample_desc = f"{cores} threads x {per} home boxes of the {b1}^3 system (x{P} particles), oracle port"
+            return len(idx)
 
-        scale = lava_cpu_scale(per, b1)
-        sample_desc += f" (home boxes 0..{per - 1}; rate scaled x{scale:.3f} to the {b1}^3 mean neighbour count)"
-
-        def work(worker, step):
-            fv = np.zeros((b1 ** 3 * P, 4))
-            g = E.GridConfig(per, P, 32, 1)
-            rc, st, msg = oracle.oracle_run(g, per, 1, E.lavamd_region(rv, qv, fv, b1, P),
-                                            make_spec(E, wl["spec"]))
-            assert rc == 0, msg
-            return per * P * scale
-    elif wl["benchmark"] == "kmeans_lloyd":
-        # random perforation is not in the reference (SPEC.md:345): the oracle
-        # port's kmeans_benchmark (same Lloyd loop and decisions) per worker
-        import ctypes as C
-        from paper_2308_16877_b200 import abi
-        d, k = wl["dims"], wl["k"]
-        per, iters = 1 << 12, 5
-        pts = E.make_blobs(per * 4, d, k, 42, wl["separation"])
-        kind = "port"
-        sample_desc = f"{cores} threads x {per} points x {iters} Lloyd iterations (oracle port kmeans_benchmark)"
-
-        def work(worker, step):
-            lo = ((worker + step) % 4) * per
-            sub = np.ascontiguousarray(pts[lo:lo + per])
-            lab = np.zeros(per, np.int32)
-            cen = np.zeros((k, d))
-            it_c, conv_c = C.c_int32(), C.c_int32()
-            stc = abi.Stats()
-            err = C.create_string_buffer(256)
-            g = E.GridConfig(per // 256, 64, 32, 4)
-            sp = make_spec(E, wl["spec"])
-            rc = oracle.oracle().oracle_kmeans_benchmark(sub.ctypes.data, per, d, k, C.byref(g.c()), C.byref(sp),
-                                                         iters, 7, lab.ctypes.data, cen.ctypes.data,
-                                                         C.byref(it_c), C.byref(conv_c), C.byref(stc), err, 256)
-            assert rc == 0, err.value
-            return per * it_c.value
-    else:
-        d, k = wl["dims"], wl["k"]
-        per = 1 << 12
-        pts = E.make_blobs(per * 4, d, k, 42, 8.0)
-        cents = pts[:k].copy()
-        sample_desc = f"{cores} threads x {per} points x {d} dims x {k} clusters, one region launch"
-
-        def work(worker, step):
-            lo = ((worker + step) % 4) * per
-            sub = np.ascontiguousarray(pts[lo:lo + per])
-            lab = np.zeros(per, np.int32)
-            g = E.GridConfig(per // 256, 64, 32, 4)
-            rc, st, msg = oracle.ref_run(g, per, 0, E.kmeans_region(sub, cents, lab), make_spec(E, wl["spec"]))
-            assert rc == 0, msg
-            return per
-
-    from concurrent.futures import ThreadPoolExecutor
-
-    def one_step(step):
         with ThreadPoolExecutor(max_workers=cores) as ex:
-            return sum(ex.map(lambda w: work(w, step), range(cores)))
+            t0 = time.perf_counter()
+            items = sum(ex.map(work, range(cores)))
+            dt = time.perf_counter() - t0
+    else:
+        # LavaMD and random perforation are not in the reference (SPEC.md:345,
+        # SURVEY Appendix C): the checker's restatement (oracle port)
+        kind = "port"
+        from concurrent.futures import ThreadPoolExecutor
+        if wl["benchmark"] == "lavamd":
+            b1, P = wl["boxes1d"], wl["particles"]
+            rv, qv = oracle.make_lavamd(b1, P, 42)
+            nb = b1 ** 3
+            grid = oracle.abi.Grid(nb, P, 32, 1, 48 * 1024)
+            mapping = 1
+            per = 4
+            sp = oracle.abi.Spec()
+            code, off = C.c_int32(), C.c_int64()
+            err = C.create_string_buffer(256)
+            oracle.ref().ref_parse_directive(wl["directive"].encode(), C.byref(sp), C.byref(code), C.byref(off), err, 256)
+            sample = f"{cores} threads x {per} interior home boxes of the {b1}^3 system, oracle port"
 
-    for s in range(args.warmup):
-        one_step(-1 - s)
-    t0 = time.perf_counter()
-    items = 0
-    for s in range(args.steps):
-        items += one_step(s)
-    dt = time.perf_counter() - t0
+            def work(w):
+                b = nb // 2 + w * per
+                fv = np.zeros((nb * P, 4))
+                reg = oracle.abi.Region()
+                reg.app, reg.output_dims, reg.lavamd_boxes1d, reg.lavamd_particles = 5, 4, b1, P
+                reg.lavamd_alpha = 0.5
+                reg.in_, reg.table_out, reg.out = rv.ctypes.data, qv.ctypes.data, fv.ctypes.data
+                rc, st, msg = oracle.oracle_run_teams(grid, nb, 1, _Raw(reg), sp, (b, b + per))
+                assert rc == 0, msg
+                return per * P
+        elif wl["benchmark"] == "kmeans":
+            # the distance region through the reference engine (kmeans.hpp:85-102)
+            kind = "reference"
+            d, k = wl["dims"], wl["k"]
+            grid, mapping = oracle.ref_grid("kmeans", wl["n"], items_per_thread=wl["ipt"])
+            m = 1 << 13
+            pts = oracle.ref_blobs(m * 4, d, k, 42, 8.0)
+            cents = np.ascontiguousarray(pts[:k])
+            sp = oracle.ref_parse(wl["directive"])
+            sub = oracle.abi.Grid(m // (64 * wl["ipt"]), 64, 32, wl["ipt"], 48 * 1024)
+            sample = f"{cores} threads x {m} points, one region launch each (reference run_region)"
+
+            def work(w):
+                x = np.ascontiguousarray(pts[(w % 4) * m:(w % 4 + 1) * m])
+                lab = np.zeros(m, np.int32)
+                reg = oracle.abi.Region()
+                reg.app, reg.kmeans_dims, reg.kmeans_k = 4, d, k
+                reg.in_, reg.centroids, reg.labels = x.ctypes.data, cents.ctypes.data, lab.ctypes.data
+                rc, st, msg = oracle.ref_run(sub, m, 0, _Raw(reg), sp)
+                assert rc == 0, msg
+                return m
+        else:
+            d, k = wl["dims"], wl["k"]
+            m, iters = 1 << 13, 5
+            grid, mapping = oracle.ref_grid("kmeans", wl["n"], items_per_thread=wl["ipt"])
+            pts = oracle.ref_blobs(m * 4, d, k, 42, wl.get("separation", 8.0))
+            sub = oracle.abi.Grid(m // 256, 64, 32, 4, 48 * 1024)
+            sp = oracle.abi.Spec()  # perfo(random:52) level(team): not reference grammar
+            sp.technique, sp.level, sp.perfo_kind, sp.perfo_skip_percent = 2, 2, 6, 52
+            sample = f"{cores} threads x {m} points x {iters} Lloyd iterations (oracle port kmeans_benchmark)"
+
+            def work(w):
+                x = np.ascontiguousarray(pts[(w % 4) * m:(w % 4 + 1) * m])
+                lab = np.zeros(m, np.int32)
+                cen = np.zeros((k, d))
+                it_c, conv_c = C.c_int32(), C.c_int32()
+                stc = oracle.abi.Stats()
+                err = C.create_string_buffer(256)
+                rc = oracle.oracle().oracle_kmeans_benchmark(x.ctypes.data, m, d, k, C.byref(sub), C.byref(sp),
+                                                             iters, 7, lab.ctypes.data, cen.ctypes.data,
+                                                             C.byref(it_c), C.byref(conv_c), C.byref(stc), err, 256)
+                assert rc == 0, err.value
+                return m * it_c.value
+
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            t0 = time.perf_counter()
+            items = sum(ex.map(work, range(cores)))
+            dt = time.perf_counter() - t0
     value = items / dt
+    # evidence that this arm ran none of the product: its package was never
+    # imported and its library never mapped
+    try:
+        mapped = any("libhpac_b200" in ln for ln in open("/proc/self/maps"))
+    except OSError:
+        mapped = None
+    extra["product_code_loaded"] = bool(mapped) or any(
+        m == "paper_2308_16877_b200" or (m.startswith("paper_2308_16877_b200.") and m != "paper_2308_16877_b200.abi")
+        for m in sys.modules)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": wl["unit"],
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / max(1, args.steps) * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["name"], "directive": wl["directive"]},
-        "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": kind,
-                         "sample": sample_desc},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the reference's generators, seed 42)",
+        "config": bench_config(wl, grid, mapping, ws),
+        "cpu_baseline": {"value": value, "unit": wl["unit"], "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **extra,
     }
     print(json.dumps(line), flush=True)
 
 
+class _Raw:
+    """A ready hpac_region_t for oracle.run_region-style helpers."""
+
+    def __init__(self, s):
+        self.s = s
+
+    def c(self):
+        return self.s
+
+
 # ------------------------------------------------------------------ our arm
 
-def cpu_baseline_sample(wl, opts, grid):
-    """Reference CPU engine on rank 0, one thread, bounded sample (~10-20 s)."""
+def cpu_baseline_sample(wl, opts, grid, ws=1):
+    """Reference CPU engine on rank 0, bounded sample (~10-20 s). Binomial:
+    the first 48 options of whole team streams on all host threads (the
+    reference arm's method, bounded); the other workloads one thread."""
     import numpy as np
 
     import oracle
     from paper_2308_16877_b200 import engine as E
+    if wl["benchmark"] == "binomial":
+        cores = host_cores()
+        r = ref_binomial_sample(wl, ws, cores, prefix=48)
+        return {"value": r["items"] / r["wall_s"], "unit": wl["unit"], "cores": r["teams"],
+                "kind": "reference", "sample": r["sample"]}
     try:
-        lib = oracle.ref()
+        oracle.ref()
         kind = "reference"
         runner = oracle.ref_run
     except Exception:
         kind = "port"
         runner = oracle.oracle_run
     t0 = time.perf_counter()
-    if wl["benchmark"] == "binomial":
-        T = grid.num_teams
-        m = 16
-        idx = 0 + np.arange(m) * T
-        sub = np.ascontiguousarray(opts[idx])
-        out = np.zeros(m)
-        rc, st, msg = runner(E.GridConfig(1, 64, 32, m), m, 1, E.binomial_region(sub, wl["lattice"], out),
-                             make_spec(E, wl["spec"]))
-        items = m
-        desc = f"team 0: {m} options (idx = s*{T}), {wl['lattice']}-step lattice, 1 thread"
-    elif wl["benchmark"] == "blackscholes":
+    if wl["benchmark"] == "blackscholes":
         m = 1 << 20
         sub = np.ascontiguousarray(opts[:m])
         out = np.zeros(m)
@@ -441,7 +585,7 @@ def cpu_baseline_sample(wl, opts, grid):
     return {"value": items / dt, "unit": wl["unit"], "cores": 1, "kind": kind, "sample": desc}
 
 
-def our_arm(args, wl):
+def our_arm(args, wl, emit=True):
     import numpy as np
     import torch
 
@@ -455,13 +599,20 @@ def our_arm(args, wl):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     n = wl.get("n")
-    spec = make_spec(E, wl["spec"])
+    spec = E.parse_directive(wl["directive"])[0]
+    team_range = None
 
-    # ---- inputs (synthetic, seeded; each rank its own shard of a ws*n job)
+    # ---- inputs (synthetic, seeded)
     seed = 42 + rank
     if wl["benchmark"] == "binomial":
-        opts = E.make_binomial_portfolio(n, seed)
+        # one global logical grid over ws x 2^20 options (the same portfolio on
+        # every rank); this rank runs a contiguous range of its teams
+        n = ws * wl["n"]
+        opts = E.make_binomial_portfolio(n, 42)
         grid, mapping = E.resolve_grid("binomial", n, items_per_thread=wl["ipt"])
+        if ws > 1:
+            T = grid.num_teams
+            team_range = (rank * T // ws, (rank + 1) * T // ws)
         d_in = torch.from_numpy(opts).to(dev)
         out_exact = torch.zeros(n, dtype=torch.float64, device=dev)
         out = torch.zeros(n, dtype=torch.float64, device=dev)
@@ -517,7 +668,8 @@ def our_arm(args, wl):
     # L2 flush buffer (> 126 MB L2), written between timed iterations
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
-    def timed_run(target, sp, steps, warmup):
+    def timed_run(target, sp, steps, warmup, g=None):
+        g = g or grid
         ts = []
         stats = None
         for i in range(warmup + steps):
@@ -530,7 +682,8 @@ def our_arm(args, wl):
             if wl["benchmark"] == "lavamd":
                 target.zero_()  # fv accumulates (Rodinia fv += ...)
             flush.zero_()
-            E.run_region(grid, n, mapping, mk(target), sp, stream=stream, synchronous=False)
+            E.run_region(g, n, mapping, mk(target), sp, stream=stream, synchronous=False,
+                         team_range=team_range if g is grid else None)
             torch.cuda.synchronize()
             st = abi.Stats()
             rc = abi.lib().hpac_stats_fetch(C.byref(st))
@@ -546,12 +699,17 @@ def our_arm(args, wl):
     clocks.start()
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < 0.6:  # untimed load so nvidia-smi sees the clocks
-        E.run_region(grid, n, mapping, mk(out), spec, stream=stream)
+        E.run_region(grid, n, mapping, mk(out), spec, stream=stream, team_range=team_range)
     ts_apx, st_apx = timed_run(out, spec, args.steps, args.warmup)
     time.sleep(0.15)
     clk = clocks.stop()
 
-    # quality loss (application metric) vs the exact run
+    # quality loss (application metric) vs the exact run; under a team-range
+    # split every rank holds the whole output array and fills its own items,
+    # so the ranks' outputs are summed (disjoint items) before the metric
+    if dist is not None and team_range is not None:
+        dist.all_reduce(out_exact)
+        dist.all_reduce(out)
     if wl["benchmark"] == "kmeans":
         quality = {"mcr": E.mcr(out_exact, out)}
         qval = quality["mcr"]
@@ -565,8 +723,20 @@ def our_arm(args, wl):
         t = torch.tensor([t_apx, t_exact], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_apx, t_exact = t.tolist()
-    value = ws * n * per_item * args.steps / (t_apx * 1e-3)
-    exact_value = ws * n * per_item * args.steps / (t_exact * 1e-3)
+    job_items = (n if team_range is not None or ws == 1 else ws * n) * per_item
+    value = job_items * args.steps / (t_apx * 1e-3)
+    exact_value = job_items * args.steps / (t_exact * 1e-3)
+
+    # ---- the exact kernel at its own best grid (binomial: ipt 256), beside the
+    # same-grid baseline above (a larger ipt gives the table more reuse but
+    # fewer, longer teams)
+    exact_best = None
+    if wl["benchmark"] == "binomial" and ws == 1 and wl.get("exact_best_ipt"):
+        g_best, _ = E.resolve_grid("binomial", n, items_per_thread=wl["exact_best_ipt"])
+        ts_b, _ = timed_run(out_exact, None, args.steps, 1, g=g_best)
+        exact_best = {"items_per_thread": wl["exact_best_ipt"], "num_teams": g_best.num_teams,
+                      "value": n * args.steps / (sum(ts_b) * 1e-3),
+                      "speedup_of_approx_over_it": value / (n * args.steps / (sum(ts_b) * 1e-3))}
 
     # ---- decision granularity comparison (C4: warp vs team, + thread)
     levels = None
@@ -602,29 +772,50 @@ def our_arm(args, wl):
             h_out = torch.zeros(n, dtype=torch.float64).pin_memory()
             hreg = (E.binomial_region(h_in.numpy(), wl["lattice"], h_out.numpy())
                     if wl["benchmark"] == "binomial" else E.blackscholes_region(h_in.numpy(), h_out.numpy()))
-        zc = E.run_region_host(grid, n, mapping, hreg, spec).stats["zero_copy"]  # warm-up
+        e2e_note = None
+        if team_range is None:
+            zc = E.run_region_host(grid, n, mapping, hreg, spec).stats["zero_copy"]  # warm-up
+
+            def e2e_step():
+                E.run_region_host(grid, n, mapping, hreg, spec)
+            e2e_items = job_items
+        else:
+            # team-range split: copy the whole portfolio in, run this rank's
+            # teams, copy the whole price array out (every rank moves n_total)
+            zc = 0
+            e2e_note = "each rank copies the whole global portfolio in and the price array out"
+
+            def e2e_step():
+                d_in.copy_(h_in, non_blocking=True)
+                E.run_region(grid, n, mapping, mk(out), spec, stream=stream, team_range=team_range)
+                h_out.copy_(out, non_blocking=True)
+                torch.cuda.synchronize()
+            e2e_step()
+            e2e_items = job_items
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            E.run_region_host(grid, n, mapping, hreg, spec)
+            e2e_step()
         e2e_t = time.perf_counter() - t0
         if dist is not None:
             t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_t = t.item()
-        e2e = {"value": ws * n * per_item * args.e2e_steps / e2e_t, "unit": wl["unit"],
+        e2e = {"value": e2e_items * args.e2e_steps / e2e_t, "unit": wl["unit"],
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
                "steps": args.e2e_steps,
                "transfer": ("zero-copy: the region kernel reads the pinned host inputs and writes the "
                             "pinned host outputs in place over PCIe" if zc else
                             "staged: H2D copy, region kernel, D2H copy")}
+        if e2e_note:
+            e2e["note"] = e2e_note
 
     if rank != 0:
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
-        return
+        return None
 
     # ---- roofline of the dominant kernel (the region kernel itself)
     peaks = measured_peaks()
@@ -669,33 +860,38 @@ def our_arm(args, wl):
     if wl["benchmark"] == "blackscholes":
         hbm_ach = roof["achieved"]
     else:
-        hbm_ach = n * per_item * bytes_item / (avg_ms * 1e-3) / 1e9
+        hbm_ach = (job_items / max(1, ws if team_range is not None else 1)) * bytes_item / (avg_ms * 1e-3) / 1e9
     roof["hbm"] = {"achieved_gbs": hbm_ach, "peak_gbs": hbm_peak, "frac": hbm_ach / hbm_peak,
                    "algorithmic": f"{bytes_item:.0f} B per item"}
 
     cpu = None
+    cpu_floor = None
     if args.cpu_baseline and ws == 1:
         try:
-            cpu = cpu_baseline_sample(wl, cpu_inputs, grid)
+            cpu = cpu_baseline_sample(wl, cpu_inputs, grid, ws)
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "unit": wl["unit"], "cores": 1, "kind": "reference",
                    "sample": f"failed: {exc}"}
+        if wl["benchmark"] == "binomial":
+            try:
+                cpu_floor = ref_binomial_floor(wl, host_cores())
+            except Exception as exc:
+                cpu_floor = {"value": None, "sample": f"failed: {exc}"}
 
+    extra = {}
     if levels:
-        extra_levels = {"decision_levels": levels}
-    else:
-        extra_levels = {}
+        extra["decision_levels"] = levels
+    if exact_best:
+        extra["exact_best_grid"] = exact_best
+    if cpu_floor:
+        extra["cpu_floor"] = cpu_floor
     line = {
         "metric": METRIC, "value": value, "unit": wl["unit"], "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generators, seed 42 + rank)",
-        "config": {"workload": wl["name"], "n_per_gpu": n * per_item, "directive": wl["directive"],
-                   "grid": {"num_teams": grid.num_teams, "threads_per_team": grid.threads_per_team,
-                            "warp_size": grid.warp_size, "items_per_thread": grid.items_per_thread},
-                   "mapping": "per-team" if mapping == 1 else "per-thread",
-                   "lattice_steps": wl.get("lattice"), "l2": "flushed between timed iterations",
-                   "parallelism": f"dp{ws} (independent shards)"},
+        "data": "synthetic (reference generators, seed 42" + (")" if team_range is not None or ws == 1
+                                                               else " + rank)"),
+        "config": bench_config(wl, grid, mapping, ws),
         "speedup_vs_exact": value / exact_value,
         "exact_value": exact_value,
         "quality": quality, "quality_ok": bool(qval <= 0.01),
@@ -705,15 +901,17 @@ def our_arm(args, wl):
         # one region kernel per step (+ the DMMA operand kernel for K-Means)
         "gpu_launches": args.steps * (2 if wl["benchmark"] == "kmeans"
                                       and kmeans_uses_dmma(wl["dims"], wl["k"]) else 1),
-        "clocks": clk, **extra_levels,
+        "clocks": clk, **extra,
     }
-    print(json.dumps(line), flush=True)
+    if emit:
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    return line
 
 
-def kmeans_lloyd_arm(args, wl):
+def kmeans_lloyd_arm(args, wl, emit=True):
     """C3: the Lloyd loop (hpac_kmeans_run) exact vs perforated on the same
     synthetic points; per-GPU shard of n points, centroid partials
     all-reduced over NCCL every iteration when N > 1 (weak scaling)."""
@@ -735,7 +933,7 @@ def kmeans_lloyd_arm(args, wl):
     # Forgy init from rank 0's first k points, identical on every rank
     cent0 = torch.from_numpy(E.make_blobs(n, d, k, 42, wl["separation"])[:k].copy() if rank else pts[:k].copy()).to(dev)
     grid, _ = E.resolve_grid("kmeans", n, items_per_thread=wl["ipt"])
-    spec = make_spec(E, wl["spec"])
+    spec = E.parse_directive(wl["directive"])[0]
     # N > 1: torch.distributed's all_reduce as the per-iteration hook (host
     # loop). BENCH_KMEANS_NATIVE_NCCL=1 uses the library's own multi-process
     # NCCL communicator instead, so the all-reduce is captured in the Lloyd
@@ -837,8 +1035,7 @@ def kmeans_lloyd_arm(args, wl):
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
-        return
-    import ctypes as C
+        return None
     from paper_2308_16877_b200 import abi
     fp = C.c_double()
     dmma = kmeans_uses_dmma(d, k)
@@ -892,13 +1089,10 @@ def kmeans_lloyd_arm(args, wl):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_a / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic make_blobs(separation {wl['separation']}), seed 42 + rank",
-        "config": {"workload": wl["name"], "n_per_gpu": n, "dims": d, "k": k, "directive": wl["directive"],
+        "config": {**bench_config(wl, grid, 0, ws), "dims": d, "k": k,
                    "max_iters": wl["max_iters"], "step": "one full Lloyd run (kmeans_benchmark)",
-                   "grid": {"num_teams": grid.num_teams, "threads_per_team": grid.threads_per_team,
-                            "warp_size": grid.warp_size, "items_per_thread": grid.items_per_thread},
-                   "l2": "flushed before every timed run; 4.3 GB of points per GPU >> L2",
-                   "timing": "sum of the region and update kernels' CUDA-event times per run",
                    "parallelism": f"dp{ws} (points sharded, NCCL all-reduce of centroid partials per iteration)"},
+        "timing": "sum of the region and update kernels' CUDA-event times per run (4.3 GB of points per GPU >> L2)",
         "speedup_vs_exact": value / exact_value,
         "time_to_solution_speedup": t_e / t_a,
         "exact_value": exact_value,
@@ -913,10 +1107,21 @@ def kmeans_lloyd_arm(args, wl):
             and spec.perfo_kind == abi.PERFO_RANDOM),
         "clocks": clk,
     }
-    print(json.dumps(line), flush=True)
+    if emit:
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    return line
+
+
+SUB_CONFIGS = ("blackscholes", "kmeans", "lavamd")  # C1, C3, C4 beside the C2 headline
+
+
+def run_workload(args, wl, emit=True):
+    if wl["benchmark"] == "kmeans_lloyd":
+        return kmeans_lloyd_arm(args, wl, emit)
+    return our_arm(args, wl, emit)
 
 
 def main():
@@ -928,14 +1133,28 @@ def main():
     ap.add_argument("--workload", default="binomial", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--sub-configs", default="auto", choices=["auto", "on", "off"],
+                    help="also measure C1/C3/C4 in this invocation and report them under `configs` "
+                         "(auto: the default binomial workload at N=1)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, wl)
-    elif wl["benchmark"] == "kmeans_lloyd":
-        kmeans_lloyd_arm(args, wl)
-    else:
-        our_arm(args, wl)
+        return
+    ws = dist_env()[0]
+    sub = args.sub_configs == "on" or (args.sub_configs == "auto" and ws == 1 and args.workload == "binomial")
+    line = run_workload(args, wl, emit=not sub)
+    if sub and line is not None:
+        sargs = argparse.Namespace(**vars(args))
+        sargs.steps, sargs.warmup, sargs.e2e_steps = max(3, args.steps // 4), max(3, min(args.warmup, 3)), 1
+        configs = {}
+        for name in SUB_CONFIGS:
+            try:
+                configs[name] = run_workload(sargs, WORKLOADS[name], emit=False)
+            except Exception as exc:  # a sub-config never takes the headline down
+                configs[name] = {"workload": WORKLOADS[name]["name"], "error": repr(exc)}
+        line["configs"] = configs
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

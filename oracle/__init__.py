@@ -88,6 +88,7 @@ def oracle():
         L.oracle_run_region_teams.argtypes = [P(abi.Grid), C.c_int64, C.c_int32, P(abi.Region), P(abi.Spec),
                                               P(abi.Stats), C.c_void_p, C.c_int32, C.c_int32, C.c_char_p,
                                               C.c_size_t]
+        L.oracle_make_lavamd.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p]
         L.oracle_bs_prices.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
         L.oracle_binomial_prices.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.oracle_arena_required.argtypes = [P(abi.Grid), P(abi.Region), P(abi.Spec), P(C.c_uint64), P(C.c_uint64), C.c_char_p, C.c_size_t]
@@ -231,6 +232,21 @@ def oracle_run_teams(grid, n, mapping, region, spec, team_range, paths=None):
                                           paths.ctypes.data if paths is not None else None,
                                           int(team_range[0]), int(team_range[1]), err, 1024)
     return rc, st, err.value.decode(errors="replace")
+
+
+def make_lavamd(b1, particles, seed):
+    n = b1 ** 3 * particles
+    rv, qv = np.empty((n, 4)), np.empty(n)
+    if oracle().oracle_make_lavamd(b1, particles, seed, rv.ctypes.data, qv.ctypes.data):
+        raise ValueError("make_lavamd: bad arguments")
+    return rv, qv
+
+
+def ref_blobs(n, dims, k, seed, separation):
+    """The reference's make_blobs (bench/kmeans.hpp:25-47)."""
+    out = np.empty((n, dims))
+    ref().ref_make_blobs(n, dims, k, seed, separation, out.ctypes.data)
+    return out
 
 
 def bs_prices(options):

@@ -449,6 +449,22 @@ static int lava_neighbours(int64_t box, int b1, int64_t* nb) {
 
 ORACLE_API double oracle_lava_exp(double x) { return lava_exp(x); }
 
+/* LavaMD inputs (the framework's definition; hpac_make_lavamd): per particle
+   rv = (v, x, y, z), qv, each (splitmix64(seed ^ (5 i + c)) % 10 + 1) / 10. */
+ORACLE_API int oracle_make_lavamd(int b1, int particles, uint64_t seed, double* rv, double* qv) {
+  if (b1 < 1 || particles < 1) return HPAC_ERR_CONFIG;
+  const int64_t n = (int64_t)b1 * b1 * b1 * particles;
+  for (int64_t i = 0; i < n; ++i)
+    for (int c = 0; c < 5; ++c) {
+      const double v = (double)(oracle_splitmix64(seed ^ (uint64_t)(5 * i + c)) % 10 + 1) / 10.0;
+      if (c < 4)
+        rv[i * 4 + c] = v;
+      else
+        qv[i] = v;
+    }
+  return 0;
+}
+
 static int region_encounters(const region_view* rv, int64_t idx) {
   if (rv->r->app == HPAC_APP_TABLE && rv->r->encounters) return rv->r->encounters[idx];
   if (rv->r->app == HPAC_APP_LAVAMD) return lava_neighbours(idx, rv->r->lavamd_boxes1d, NULL);

@@ -363,7 +363,7 @@ using LatBlocks = BList<33, 28, 24, 20, 17, 14, 12, 10, 8, 7, 6, 5, 4, 3, 2, 1>;
 template <int B, int BMAX>
 __device__ __forceinline__ void bt_phase(double (&v)[BMAX], int& L, int lo, int pmax,
                                          const LatParams& q, int lane, double* xch, bool check,
-                                         bool& ok, int& nex, int top) {
+                                         bool& ok, int& nex, int top, double eps_k, int& jsig) {
   const int base = lo + lane * B;
   // nodes above `top` (= N+1) are dead: never loaded from or stored to xch
 #pragma unroll
@@ -397,8 +397,10 @@ __device__ __forceinline__ void bt_phase(double (&v)[BMAX], int& L, int lo, int 
     x0 = fma(x0, q.up, q.c1);
     --L;
   }
-  // exercised prefix length at the last level processed (boundary estimate)
+  // exercised prefix length at the last level processed (boundary estimate),
+  // and the highest node there whose value is still significant (> eps*K)
   int cnt = 0;
+  int js = -1;
   {
     double xa = x0_last, xb = fma(x0_last, q.up2, q.c2);
 #pragma unroll
@@ -412,9 +414,11 @@ __device__ __forceinline__ void bt_phase(double (&v)[BMAX], int& L, int lo, int 
         xb = fma(xb, q.up4, q.c4);
       }
       if (base + i <= L_last && v[i] == x) ++cnt;
+      if (base + i <= L_last && base + i <= top && v[i] > eps_k) js = base + i;
     }
   }
   nex = __reduce_add_sync(0xffffffffu, cnt);
+  jsig = __reduce_max_sync(0xffffffffu, js);
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < B; ++i)
@@ -432,6 +436,10 @@ __device__ __forceinline__ void bt_fill_exercise(double* xch, int from, int to, 
 // Returns false (caller recomputes the full triangle) when a boundary check
 // fails or the continuation region outgrows the compiled block sizes.
 constexpr int kBtBmax = 20;
+#ifndef HPAC_BT_TAIL_EPS
+#define HPAC_BT_TAIL_EPS 1e-16
+#endif
+constexpr double kBtTailEps = HPAC_BT_TAIL_EPS;  // relative to the strike
 
 template <bool AM, bool PUT>
 __device__ double lattice_smem_inplace(double spot, double strike, int N, const LatParams& q,
@@ -439,7 +447,8 @@ __device__ double lattice_smem_inplace(double spot, double strike, int N, const 
 
 template <int BMAX>
 __device__ bool binomial_put_bt(double spot, double strike, int N, const LatParams& q,
-                                double* xch, double& price, unsigned long long& nodes) {
+                                double* xch, double& price, unsigned long long& nodes,
+                                bool cut_tail) {
   const int lane = threadIdx.x & 31;
   constexpr int kPhase = 32;   // levels per phase
   constexpr int kMargin = 8;   // nodes kept below the measured boundary
@@ -465,7 +474,20 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
   // is exactly +0 at every level (0*p + 0*q = +0). The live range is capped
   // at jk (+ the zero right neighbour jk+1): the upper quarter of the
   // triangle is never computed, and every computed node is unchanged.
-  const int top = jk + 1;
+  //
+  // Negligible tail: the set of nodes above an index J whose values are all
+  // <= eps*K is closed under backward induction (node j at level L reads
+  // only j and j+1 at L+1; above the strike node the exercise value is
+  // negative, so the max is the discounted average, <= eps*K again). So at
+  // the end of every phase the cap `hi` drops to the highest node still
+  // above eps*K; the node hi+1 continues with a zero right neighbour. Each
+  // level that changes the root by at most eps*K (the backward operator is
+  // a sup-norm contraction), so the price moves by <= N*eps*K in total:
+  // ~1e-13 K at N = 1024 with eps = 1e-16, far inside the 1e-6 exact-path
+  // tolerance, while ~40 % of the remaining nodes (the far out-of-the-money
+  // tail whose values underflow towards 0) are never computed.
+  int hi = jk;
+  const double eps_k = kBtTailEps * strike;
   if (jk < lo) {
     // no in-the-money leaf at or above the bound: with lo == 0 every node is
     // exactly 0; otherwise let the full lattice handle it
@@ -478,17 +500,18 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
   }
   int L = N - 1;
   while (L >= 0) {
-    const int live = min(L, jk) + 2 - lo;
+    const int top = hi + 1;
+    const int live = min(L, hi) + 2 - lo;
     if (live > 32 * kBtMax || live < 1) return false;
     {
-      const int lv = min(L + 1, kPhase);  // levels L .. L-lv+1 over nodes lo..min(level, jk)
-      for (int t = 0; t < lv; ++t) nodes += (unsigned long long)(min(L - t, jk) + 1 - lo);
+      const int lv = min(L + 1, kPhase);  // levels L .. L-lv+1 over nodes lo..min(level, hi)
+      for (int t = 0; t < lv; ++t) nodes += (unsigned long long)max(0, min(L - t, hi) + 1 - lo);
     }
     bool ok = true;
-    int nex = 0;
+    int nex = 0, jsig = hi;
     const bool check = lo > 0;
 #define HPAC_BT(b, bn) \
-  if (live > 32 * (bn)) { bt_phase<b, BMAX>(v, L, lo, kPhase, q, lane, xch, check, ok, nex, top); } else
+  if (live > 32 * (bn)) { bt_phase<b, BMAX>(v, L, lo, kPhase, q, lane, xch, check, ok, nex, top, eps_k, jsig); } else
     // 11 block sizes (13 before the 8-CTA/SM change: with more warps per SM
     // sharing the instruction cache, fewer instantiations beat tighter fits;
     // 9 and 7 sizes measured 0.5 % and 6 % slower)
@@ -497,6 +520,9 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
 #undef HPAC_BT
     if (!__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) return false;
     if (L < 0) break;
+    // the tail above the last significant node stays negligible (never below
+    // the boundary bound: those nodes are exercised, hence significant)
+    if (cut_tail) hi = max(min(hi, jsig), lo);
     // next bound: measured boundary (level L+1) minus margin and half a phase
     // of drift; never above mid-lattice; full range near the root
     int lo_new = lo + nex - kMargin - kPhase / 2;
@@ -551,7 +577,16 @@ __device__ double binomial_warp_price(const double* o, int N, double* xch, bool&
     // shared memory if its checks fail (keeps the hot kernel small)
     double price;
     unsigned long long nodes = 0;
-    if (binomial_put_bt<kBtBmax>(spot, strike, N, q, xch, price, nodes)) {
+    // the tail cut moves the price by at most N*eps*K (binomial_put_bt); when
+    // that is not below 1e-9 of the price itself (tiny, far out-of-the-money
+    // prices) the lattice is recomputed without it (one call site: the hot
+    // code is instantiated once)
+    bool done = false;
+    for (int pass = 0; pass < 2; ++pass) {
+      done = binomial_put_bt<kBtBmax>(spot, strike, N, q, xch, price, nodes, pass == 0);
+      if (!done || price * 1e-9 >= (double)N * kBtTailEps * strike) break;
+    }
+    if (done) {
       if (lane == 0 && fallbacks) atomicAdd(fallbacks + 1, nodes);
       return price;
     }

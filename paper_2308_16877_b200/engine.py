@@ -389,14 +389,22 @@ def kmeans_run(grid: GridConfig, points, k, spec=None, max_iters=40, centroids=N
         pb.allreduce_user = nccl_comm
     elif allreduce is not None:
         def _cb(buf, count, user, st):
-            # The library produced `red` on stream `st` and reads it back there:
-            # run the collective on that same stream (torch orders NCCL against
-            # its current stream). An exception cannot cross the C boundary, so
-            # it is kept, reported as a nonzero status (the loop stops with
-            # HPAC_ERR_CUDA) and re-raised below.
+            # The library produced `red` on stream `st` and reads it back there,
+            # while torch orders the collective against its current stream:
+            # when the two differ, torch's stream waits for `st` before the
+            # all-reduce and `st` waits for torch's stream after it. An
+            # exception cannot cross the C boundary, so it is kept, reported as
+            # a nonzero status (the loop stops with HPAC_ERR_CUDA) and
+            # re-raised below.
             try:
-                with torch.cuda.stream(torch.cuda.ExternalStream(st or 0, device=points.device)):
-                    allreduce(red)
+                cur = torch.cuda.current_stream(points.device)
+                lib_stream = torch.cuda.ExternalStream(st, device=points.device) \
+                    if st and st != cur.cuda_stream else None
+                if lib_stream is not None:
+                    cur.wait_stream(lib_stream)
+                allreduce(red)
+                if lib_stream is not None:
+                    lib_stream.wait_stream(cur)
                 return 0
             except BaseException as exc:  # noqa: BLE001 - re-raised after the run
                 hook_error.append(exc)

@@ -27,4 +27,4 @@ def test_bench_two_ranks(workload, port):
     assert len(lines) == 1  # rank 0 alone prints
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
-    assert d["quality_ok"]
+    assert d["quality_ok"], lines[0][:3000]

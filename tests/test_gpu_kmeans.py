@@ -280,3 +280,24 @@ def test_lloyd_cluster_losing_half_its_points():
             mcr = float((r.assignments.cpu().numpy() != want_a).mean())
             assert mcr <= 1e-3, mcr
             assert np.allclose(r.centroids.cpu().numpy(), want_c, rtol=1e-9, atol=1e-9)
+
+
+def test_python_hook_on_a_non_current_stream():
+    """kmeans_run on a stream that is not torch's current stream: the hook's
+    collective (ordered by torch against its current stream) must still see
+    the finished partials and be seen by the library's readback (ADVICE r01:
+    stream ordering of the torch.distributed hook)."""
+    pts = E.make_blobs(8192, 8, 16, 5, 12.0)
+    grid, _ = E.resolve_grid("kmeans", 8192)
+    single = E.kmeans_run(grid, dev(pts), 16, host_loop=True)
+    side = torch.cuda.Stream()
+
+    def doubled(buf):
+        torch.cuda._sleep(2_000_000)  # a slow collective on torch's current stream
+        buf.mul_(2.0)
+
+    r = E.kmeans_run(grid, dev(pts), 16, allreduce=doubled, stream=side)
+    torch.cuda.synchronize()
+    assert r.iterations == single.iterations
+    assert torch.equal(r.assignments, single.assignments)
+    assert torch.equal(r.centroids, single.centroids)
