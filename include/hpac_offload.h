@@ -332,6 +332,18 @@ int hpac_probe_fp64_peak(double* tflops);
 /* FP64 tensor-op (DMMA m8n8k4) peak, TFLOP/s: the K-Means DMMA filter's roofline. */
 int hpac_probe_dmma_peak(double* tflops);
 
+/* ---- diagnostics ------------------------------------------------------ */
+/* Evaluate one of the accurate-path math functions element-wise on device
+   buffers (test support for csrc/fastmath.cuh; no reference counterpart).
+   The BS kinds read AoS option records (5 doubles per element; n records)
+   and write NaN where black_scholes_call would throw. */
+enum {
+  HPAC_FM_EXP = 0, HPAC_FM_LOG = 1, HPAC_FM_ERFC = 2, HPAC_FM_BS = 3,
+  HPAC_FM_LIBDEVICE_EXP = 4, HPAC_FM_LIBDEVICE_LOG = 5, HPAC_FM_LIBDEVICE_ERFC = 6,
+  HPAC_FM_LIBDEVICE_BS = 7
+};
+int hpac_fm_eval(int32_t kind, const double* x, double* y, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -121,6 +121,7 @@ def _declare(lib):
         "hpac_nccl_comm_init_rank": (C.c_int, [C.c_int, C.c_char_p, C.c_int, P(C.c_void_p)]),
         "hpac_probe_dmma_peak": (C.c_int, [P(C.c_double)]),
         "hpac_make_lavamd": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
+        "hpac_fm_eval": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -6,31 +6,50 @@
 #include <cstdint>
 
 #include "engine.h"
+#include "fastmath.cuh"
 #include "hpac_device.cuh"
 
 namespace hpac {
 
 // black_scholes_call, bench/blackscholes.hpp:21-36. Returns false where the
-// reference throws ConfigError (invalid parameters).
+// reference throws ConfigError (invalid parameters). The transcendental
+// functions are csrc/fastmath.cuh's (<= 1 ulp exp/log, <= 4 ulp erfc, the
+// libdevice bounds, at about half libdevice's instruction count).
 __device__ __forceinline__ bool bs_call(double spot, double strike, double rate, double vol,
                                         double mat, double& price) {
   if (!(spot > 0) || !(strike > 0) || !(mat > 0) || !(vol >= 0) || !isfinite(rate))
     return false;
-  double disc_strike = strike * exp(-rate * mat);
+  double disc_strike = strike * fm::exp(-rate * mat);
   double sst = vol * sqrt(mat);
   if (sst == 0.0) {
     double v = spot - disc_strike;
     price = v < 0.0 ? 0.0 : v;
     return true;
   }
-  double d1 = (log(spot / strike) + (rate + 0.5 * vol * vol) * mat) / sst;
+  double d1 = fm::div(fm::log(fm::div(spot, strike)) + (rate + 0.5 * vol * vol) * mat, sst);
   double d2 = d1 - sst;
   // norm_cdf(x) = erfc(-x/sqrt2)/2 (blackscholes.hpp:21); the division by
   // sqrt2 is a multiplication by -1/sqrt2 here (<= 1 ulp in the argument)
-  double n1 = 0.5 * erfc(d1 * -0.70710678118654752440);
-  double n2 = 0.5 * erfc(d2 * -0.70710678118654752440);
+  double n1 = 0.5 * fm::erfc(d1 * -0.70710678118654752440);
+  double n2 = 0.5 * fm::erfc(d2 * -0.70710678118654752440);
   price = spot * n1 - disc_strike * n2;
   return true;
+}
+
+// The same formula on libdevice's exp/log/erfc and IEEE division (the
+// round-1 kernel); kept for the device accuracy test (hpac_fm_eval).
+__device__ __forceinline__ double bs_call_libdevice(double spot, double strike, double rate,
+                                                    double vol, double mat) {
+  double disc_strike = strike * ::exp(-rate * mat);
+  double sst = vol * sqrt(mat);
+  if (sst == 0.0) {
+    double v = spot - disc_strike;
+    return v < 0.0 ? 0.0 : v;
+  }
+  double d1 = (::log(spot / strike) + (rate + 0.5 * vol * vol) * mat) / sst;
+  double d2 = d1 - sst;
+  return spot * (0.5 * ::erfc(d1 * -0.70710678118654752440)) -
+         disc_strike * (0.5 * ::erfc(d2 * -0.70710678118654752440));
 }
 
 // Hooks every app inherits: encounters per item (Region::encounters,
@@ -124,6 +143,7 @@ struct AppBlackScholes : AppBase {
     if (p.region.out) __stcs(p.region.out + idx, out[0]);
   }
 };
+
 
 // K-Means distance region (bench/kmeans.hpp:82-102). The region's outputs
 // are the k distances; the host argmin (kmeans.hpp:111-121) is fused here,

@@ -61,6 +61,10 @@ struct EngineParams {
   int32_t smem_ctl_off;   // control words (int, counts)
   int32_t ctl_ints;
   int32_t lat_bmax;       // binomial: register block bound
+  // Blackscholes iACT engine (engine_bs_iact.cu): lookups decide a chunk of
+  // q_steps steps, then the CTA prices the queued misses densely
+  int32_t q_steps;
+  double iact_thr2;       // largest ssq with sqrt_rn(ssq) <= iact_thr (exact test, no sqrt)
   // outputs
   uint8_t* paths;
   unsigned long long* counters;

@@ -22,9 +22,13 @@
 // technique none / TAF (h <= 8) / perforation.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "apps.cuh"
 #include "engine.h"
 #include "hpac_device.cuh"
+#include "tma.cuh"
 
 namespace hpac {
 
@@ -33,40 +37,6 @@ namespace {
 constexpr int kStreamMaxT = 256;
 constexpr int kTechNoneStream = 3;  // accurate baseline (spec == NULL)
 constexpr int kRec = 5;  // doubles per option record
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 __device__ __forceinline__ unsigned long long warp_sum_u32(unsigned v) {
   unsigned long long s = v;
@@ -77,118 +47,150 @@ __device__ __forceinline__ unsigned long long warp_sum_u32(unsigned v) {
 
 }  // namespace
 
-template <int TECH, int LEVEL, int HREG>
-__global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_kernel(const EngineParams p) {
+// One CUDA thread runs PAIR logical threads of the team: local and
+// local + tpt/PAIR (both in hardware-aligned 32-lane segments, so warp votes
+// stay segment ballots per logical set). Two independent options per thread
+// double the FP64 instruction-level parallelism of the accurate path (the
+// kernel is latency-bound on DFMA chains at one option per thread) and halve
+// the per-option share of the step bookkeeping.
+template <int TECH, int LEVEL, int HREG, int PAIR>
+__global__ void __launch_bounds__(kStreamMaxT / PAIR, (PAIR == 2 ? 4 : 3))
+    bs_stream_kernel(const EngineParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tpt = p.tpt;
+  const int half = tpt / PAIR;  // physical threads
   double* tile = smem;                                             // [2][tpt*5]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * tpt * kRec);  // [2]
 
-  const int local = threadIdx.x;
+  const int phys = threadIdx.x;
   const int team = p.team_begin + (int)blockIdx.x;
-  const int64_t tid = (int64_t)team * tpt + local;
   const int64_t G = p.stride;
   const int ws = p.ws;
-  const int lane = local % ws;
-  const int hw_lane = local & 31;
+  const int hw_lane = phys & 31;
+  const int lane = hw_lane % ws;  // logical lane (half is a multiple of 32)
   const unsigned seg_mask = ws >= 32 ? 0xffffffffu : (((1u << ws) - 1u) << (hw_lane - lane));
   const double* __restrict__ in = p.region.in;
   double* __restrict__ out = p.region.out;
   const int64_t team_base = (int64_t)team * tpt;
+  // per-team schedule bounds, once: steps [0, full) see a whole tile, step
+  // `full` (if < tsteps) a ragged one, steps >= tsteps nothing
+  const int64_t rem0 = p.n - team_base;  // items at or after this team's step-0 base
+  const int tsteps = rem0 <= 0 ? 0 : (int)(p.steps < (rem0 - 1) / G + 1 ? p.steps : (rem0 - 1) / G + 1);
+  const int full = rem0 < tpt ? 0 : (int)(p.steps < (rem0 - tpt) / G + 1 ? p.steps : (rem0 - tpt) / G + 1);
+  const int ragged = tsteps > full ? (int)(rem0 - (int64_t)full * G) : 0;  // count at step `full`
+  const int nsteps = (int)p.steps;
   // bulk copies need 16-byte aligned source and size: tpt*40 B per tile is a
   // multiple of 16 when tpt is even (always, tpt % 32 == 0); the ragged last
   // tile of the grid and misaligned buffers fall back to per-thread loads.
   const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  auto tile_count = [&](int s) -> int { return s < full ? tpt : (s == full ? ragged : 0); };
+  auto tile_tma = [&](int s) -> bool { return aligned && s < full; };
+  const uint32_t tile_bytes = (uint32_t)(tpt * kRec * 8);
 
-  auto tile_count = [&](int64_t s) -> int {
-    const int64_t b = team_base + s * G;
-    const int64_t c = p.n - b;
-    return c <= 0 ? 0 : (c >= tpt ? tpt : (int)c);
-  };
-  auto tile_tma = [&](int64_t s) -> bool {
-    return aligned && s < p.steps && tile_count(s) == tpt;
-  };
-
-  if (local == 0) {
+  if (phys == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_fence_init();
   }
   __syncthreads();
   uint32_t phase0 = 0, phase1 = 0;
-  if (local == 0 && p.steps > 0 && tile_tma(0)) {
-    mbar_expect_tx(&bar[0], (uint32_t)(tpt * kRec * 8));
-    tma_load_1d(tile, in + team_base * kRec, (uint32_t)(tpt * kRec * 8), &bar[0]);
+  bool loaded_cur = nsteps > 0 && tile_tma(0);
+  if (phys == 0 && loaded_cur) {
+    mbar_expect_tx(&bar[0], tile_bytes);
+    tma_load_1d(tile, in + team_base * kRec, tile_bytes, &bar[0]);
   }
-  bool loaded_cur = p.steps > 0 && tile_tma(0);
   // thread 0's bookkeeping: a load into buffer b that no consumer waited for
   // is still "outstanding"; it must be retired before the buffer is re-armed
   // (an mbarrier must not see a second arrive while its phase is pending)
   bool issued0 = loaded_cur, issued1 = false;
 
-  // TAF state (TafState, taf.hpp:59-163): register shift register, oldest first
-  int taf_mode = kTafFilling, taf_rem = 0, taf_count = 0;
-  double win[HREG > 0 ? HREG : 1];
+  // per logical thread k: local = phys + k*half, tid = team_base + local
+  constexpr int HW = HREG > 0 ? HREG : 1;
+  int taf_mode[PAIR], taf_rem[PAIR], taf_count[PAIR];
+  double win[PAIR][HW], last[PAIR];
+  int trip[PAIR];
 #pragma unroll
-  for (int i = 0; i < (HREG > 0 ? HREG : 1); ++i) win[i] = 0.0;
-  double last = 0.0;
-  int64_t trip = 0;
-  if (TECH == HPAC_TECH_PERFO &&
-      (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
-    trip = trip_count(tid, G, p.n, p.steps);
+  for (int k = 0; k < PAIR; ++k) {
+    taf_mode[k] = kTafFilling;
+    taf_rem[k] = 0;
+    taf_count[k] = 0;
+    last[k] = 0.0;
+#pragma unroll
+    for (int i = 0; i < HW; ++i) win[k][i] = 0.0;
+    trip[k] = 0;
+    if (TECH == HPAC_TECH_PERFO &&
+        (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
+      trip[k] = (int)trip_count(team_base + phys + k * half, G, p.n, p.steps);
+  }
 
-  unsigned c_total = 0, c_approx = 0, c_warp = 0, c_div = 0;
-  bool touched = false, app_error = false;
+  unsigned c_total = 0, c_approx = 0, c_warp = 0, c_div = 0, c_res = 0;
+  bool app_error = false;
+  const double* src_step = in + (team_base + phys) * kRec;  // logical 0's record at step s
+  double* dst_step = out ? out + team_base + phys : nullptr;
+  uint8_t* path_step = p.paths ? p.paths + team_base + phys : nullptr;
 
-  for (int64_t step = 0; step < p.steps; ++step) {
+  for (int step = 0; step < nsteps; ++step) {
     const int cnt = tile_count(step);
-    const bool active = local < cnt;  // idx = tid + step*G < n
-    const int64_t idx = tid + step * G;
-    const int buf = (int)(step & 1);
-
-    // ---- predicate (engine.hpp:221-251); for 1-encounter regions the
-    // per-thread and herded perforation counters both equal `step`
-    bool pred = false;
-    if (active) {
-      if (TECH == HPAC_TECH_TAF) pred = taf_mode == kTafPredicting;
-      if (TECH == HPAC_TECH_PERFO)
-        pred = perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, step,
-                                 trip, tid);
-    }
-    // known approximate at step+1 (thread level decisions only depend on
-    // the thread's own state; any approximate lane needs no input)
+    const int buf = step & 1;
+    bool active[PAIR], pred[PAIR], approx[PAIR];
     bool need_next = false;
-    if (step + 1 < p.steps && local < tile_count(step + 1)) {
-      need_next = true;
-      if (TECH == HPAC_TECH_TAF && LEVEL == HPAC_LEVEL_THREAD)
-        need_next = !(taf_mode == kTafPredicting && taf_rem >= 2);
-      if (TECH == HPAC_TECH_PERFO)
-        need_next = !perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed,
-                                       step + 1, trip, tid);
+    const int cnt_next = tile_count(step + 1);
+#pragma unroll
+    for (int k = 0; k < PAIR; ++k) {
+      const int local = phys + k * half;
+      const int64_t tid = team_base + local;
+      active[k] = local < cnt;  // idx = tid + step*G < n
+      // ---- predicate (engine.hpp:221-251); for 1-encounter regions the
+      // per-thread and herded perforation counters both equal `step`
+      pred[k] = false;
+      if (active[k]) {
+        if (TECH == HPAC_TECH_TAF) pred[k] = taf_mode[k] == kTafPredicting;
+        if (TECH == HPAC_TECH_PERFO)
+          pred[k] = perfo_should_skip32(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, step,
+                                        trip[k], tid);
+      }
+      // known approximate at step+1 (thread level decisions only depend on
+      // the thread's own state; any approximate lane needs no input)
+      if (step + 1 < nsteps && local < cnt_next) {
+        bool nn = true;
+        if (TECH == HPAC_TECH_TAF && LEVEL == HPAC_LEVEL_THREAD)
+          nn = !(taf_mode[k] == kTafPredicting && taf_rem[k] >= 2);
+        if (TECH == HPAC_TECH_PERFO)
+          nn = !perfo_should_skip32(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, step + 1,
+                                    trip[k], tid);
+        need_next = need_next || nn;
+      }
+      approx[k] = pred[k];
     }
 
     // ---- team barrier: frees tile[buf^1] (consumed at step-1), team vote,
-    // and "does anybody need the next tile" in one or two bar.red ops
-    bool approx = pred;
+    // and "does anybody need the next tile" in bar.red ops
     if (TECH != kTechNoneStream && LEVEL == HPAC_LEVEL_TEAM) {
-      const int yes = __syncthreads_count(active && pred);
-      approx = 2 * yes > cnt;  // majority_decision over the team's active threads
+      int yes = 0;
+#pragma unroll
+      for (int k = 0; k < PAIR; ++k) yes += __syncthreads_count(active[k] && pred[k]);
+      const bool ta = 2 * yes > cnt;  // majority_decision over the team's active threads
+#pragma unroll
+      for (int k = 0; k < PAIR; ++k) approx[k] = ta;
     }
     const int any_next = __syncthreads_or(need_next);
     if (LEVEL == HPAC_LEVEL_WARP && TECH != kTechNoneStream) {
-      const unsigned bv = __ballot_sync(0xffffffffu, active && pred) & seg_mask;
-      const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
-      approx = 2 * __popc(bv) > __popc(ba);
+#pragma unroll
+      for (int k = 0; k < PAIR; ++k) {
+        const unsigned bv = __ballot_sync(0xffffffffu, active[k] && pred[k]) & seg_mask;
+        const unsigned ba = __ballot_sync(0xffffffffu, active[k]) & seg_mask;
+        approx[k] = 2 * __popc(bv) > __popc(ba);
+      }
     }
     bool loaded_next = false;
     if (any_next && tile_tma(step + 1)) {
       loaded_next = true;
-      if (local == 0) {
+      if (phys == 0) {
         const int nb = buf ^ 1;
         if (nb ? issued1 : issued0) mbar_wait(&bar[nb], (nb ? phase1 : phase0) ^ 1);
-        mbar_expect_tx(&bar[nb], (uint32_t)(tpt * kRec * 8));
-        tma_load_1d(tile + nb * tpt * kRec, in + (team_base + (step + 1) * G) * kRec,
-                    (uint32_t)(tpt * kRec * 8), &bar[nb]);
+        mbar_expect_tx(&bar[nb], tile_bytes);
+        tma_load_1d(tile + nb * tpt * kRec, in + (team_base + (int64_t)(step + 1) * G) * kRec,
+                    tile_bytes, &bar[nb]);
         if (nb)
           issued1 = true;
         else
@@ -196,60 +198,96 @@ __global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_ker
       }
     }
 
-    // ---- lane execution (engine.hpp:303-347)
-    if (active) {
-      if (approx) {
+    // ---- lane execution (engine.hpp:303-347): both logical threads' inputs
+    // first, then both evaluations in one straight-line block
+    bool ev[PAIR];
+    bool any_ev = false;
+#pragma unroll
+    for (int k = 0; k < PAIR; ++k) {
+      ev[k] = active[k] && !approx[k];
+      any_ev = any_ev || ev[k];
+    }
+    double v[PAIR];
+#pragma unroll
+    for (int k = 0; k < PAIR; ++k) v[k] = 0.0;
+    if (any_ev) {
+      double rec[PAIR][kRec];
+      if (loaded_cur) {
+        mbar_wait(&bar[buf], buf ? phase1 : phase0);
+#pragma unroll
+        for (int k = 0; k < PAIR; ++k) {
+          const double* t = tile + buf * tpt * kRec + (phys + k * half) * kRec;
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) rec[k][c] = t[c];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PAIR; ++k) {
+          const double* o = src_step + (int64_t)k * half * kRec;
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) rec[k][c] = ev[k] ? __ldg(o + c) : 1.0;
+        }
+      }
+      // an approximate or inactive logical thread prices a dummy valid
+      // option (1,1,0,0,1) alongside; its result is discarded
+#pragma unroll
+      for (int k = 0; k < PAIR; ++k)
+        if (!ev[k]) {
+          rec[k][0] = 1.0;
+          rec[k][1] = 1.0;
+          rec[k][2] = 0.0;
+          rec[k][3] = 0.0;
+          rec[k][4] = 1.0;
+        }
+#pragma unroll
+      for (int k = 0; k < PAIR; ++k)
+        if (!bs_call(rec[k][0], rec[k][1], rec[k][2], rec[k][3], rec[k][4], v[k]) && ev[k])
+          app_error = true;
+    }
+
+#pragma unroll
+    for (int k = 0; k < PAIR; ++k) {
+      if (!active[k]) continue;
+      double* o = dst_step ? dst_step + (int64_t)k * half : nullptr;
+      if (approx[k]) {
         if (TECH == HPAC_TECH_TAF) {
           // TafState::emit_approx, taf.hpp:114-117
-          if (out) __stcs(out + idx, last);
-          if (taf_mode == kTafPredicting && --taf_rem == 0) {
-            taf_count = 0;
-            taf_mode = kTafFilling;
+          if (o) __stcs(o, last[k]);
+          if (taf_mode[k] == kTafPredicting && --taf_rem[k] == 0) {
+            taf_count[k] = 0;
+            taf_mode[k] = kTafFilling;
           }
         }
         // perforation: output untouched
       } else {
-        double rec[kRec];
-        if (loaded_cur) {
-          mbar_wait(&bar[buf], buf ? phase1 : phase0);
-          const double* t = tile + buf * tpt * kRec + local * kRec;
-#pragma unroll
-          for (int c = 0; c < kRec; ++c) rec[c] = t[c];
-        } else {
-          const double* o = in + idx * kRec;
-#pragma unroll
-          for (int c = 0; c < kRec; ++c) rec[c] = __ldg(o + c);
-        }
-        double v = 0.0;
-        if (!bs_call(rec[0], rec[1], rec[2], rec[3], rec[4], v)) app_error = true;
-        if (out) __stcs(out + idx, v);
+        if (o) __stcs(o, v[k]);
         if (TECH == HPAC_TECH_TAF) {
           // TafState::observe_accurate, taf.hpp:94-108
 #pragma unroll
-          for (int i = 0; i + 1 < (HREG > 0 ? HREG : 1); ++i) win[i] = win[i + 1];
-          win[(HREG > 0 ? HREG : 1) - 1] = v;
-          if (taf_count < HREG) ++taf_count;
-          last = v;
-          const bool check =
-              (taf_mode == kTafFilling && taf_count == HREG) || taf_mode == kTafChecking;
-          if (taf_mode == kTafPredicting) {
-            if (--taf_rem == 0) {
-              taf_count = 0;
-              taf_mode = kTafFilling;
+          for (int i = 0; i + 1 < HW; ++i) win[k][i] = win[k][i + 1];
+          win[k][HW - 1] = v[k];
+          if (taf_count[k] < HREG) ++taf_count[k];
+          last[k] = v[k];
+          const bool check = (taf_mode[k] == kTafFilling && taf_count[k] == HREG) ||
+                             taf_mode[k] == kTafChecking;
+          if (taf_mode[k] == kTafPredicting) {
+            if (--taf_rem[k] == 0) {
+              taf_count[k] = 0;
+              taf_mode[k] = kTafFilling;
             }
           } else if (check) {
-            if (taf_window_passes<(HREG > 0 ? HREG : 1)>(win, p.taf_thr)) {
-              taf_rem = p.taf_p;
-              taf_mode = kTafPredicting;
+            if (taf_window_passes<HW>(win[k], p.taf_thr)) {
+              taf_rem[k] = p.taf_p;
+              taf_mode[k] = kTafPredicting;
             } else {
-              taf_mode = kTafChecking;
+              taf_mode[k] = kTafChecking;
             }
           }
         }
       }
       c_total += 1;
-      if (approx) c_approx += 1;
-      if (p.paths) p.paths[idx] = approx ? 1 : 0;
+      if (approx[k]) c_approx += 1;
+      if (path_step) path_step[(int64_t)k * half] = approx[k] ? 1 : 0;
     }
     // every thread observes the completion of a loaded tile it did not read,
     // so the buffer's phase stays in step for the whole team
@@ -261,19 +299,25 @@ __global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_ker
     }
     loaded_cur = loaded_next;
 
-    // ---- warp stats (cost.hpp:66-86)
-    const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
-    const unsigned bx = __ballot_sync(0xffffffffu, active && approx) & seg_mask;
-    if (lane == 0 && ba) {
-      touched = true;
-      c_warp += 1;
-      if (bx != 0 && bx != ba) c_div += 1;
+    // ---- warp stats (cost.hpp:66-86), per logical set
+#pragma unroll
+    for (int k = 0; k < PAIR; ++k) {
+      const unsigned ba = __ballot_sync(0xffffffffu, active[k]) & seg_mask;
+      const unsigned bx = __ballot_sync(0xffffffffu, active[k] && approx[k]) & seg_mask;
+      if (lane == 0 && ba) {
+        c_res |= 1u << k;
+        c_warp += 1;
+        if (bx != 0 && bx != ba) c_div += 1;
+      }
     }
+    src_step += G * kRec;
+    if (dst_step) dst_step += G;
+    if (path_step) path_step += G;
   }
   // a tile may have been fetched speculatively and then not read by anybody
   // (every lane approximated): thread 0 retires the last copy of each
   // buffer so none is in flight when the CTA exits
-  if (local == 0) {
+  if (phys == 0) {
     if (issued0) mbar_wait(&bar[0], phase0 ^ 1);
     if (issued1) mbar_wait(&bar[1], phase1 ^ 1);
   }
@@ -282,7 +326,7 @@ __global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_ker
   const unsigned long long s_approx = warp_sum_u32(c_approx);
   const unsigned long long s_warp = warp_sum_u32(c_warp);
   const unsigned long long s_div = warp_sum_u32(c_div);
-  const unsigned long long s_res = warp_sum_u32((lane == 0 && touched) ? 1u : 0u);
+  const unsigned long long s_res = warp_sum_u32(__popc(c_res));
   const unsigned any_err = __ballot_sync(0xffffffffu, app_error);
   if (hw_lane == 0) {
     if (s_total) atomicAdd(&p.counters[kCntTotal], s_total);
@@ -297,6 +341,7 @@ __global__ void __launch_bounds__(kStreamMaxT, (HREG > 5 ? 3 : 4)) bs_stream_ker
 bool engine_stream_eligible(const EngineParams& p) {
   if (p.region.app != HPAC_APP_BLACKSCHOLES) return false;
   if (p.per_team || p.has_enc || p.barrier_eval || p.staged) return false;
+  if (p.steps >= 0x7fffffff) return false;  // 32-bit step counters
   if (!p.fast_ws || p.tpt % 32 != 0 || p.tpt > kStreamMaxT) return false;
   if (p.tech == HPAC_TECH_IACT) return false;
   if (p.tech == HPAC_TECH_TAF && p.taf_h > 8) return false;
@@ -307,19 +352,33 @@ size_t engine_stream_smem(const EngineParams& p) {
   return (size_t)2 * p.tpt * kRec * sizeof(double) + 2 * sizeof(uint64_t);
 }
 
+template <int TECH, int LEVEL, int H>
+static void stream_launch_h(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st) {
+  // two logical threads per CUDA thread (tpt % 64 == 0) only on request
+  // (HPAC_STREAM_PAIR=1): measured 97.0 us unpaired vs 98.6 us paired on C1
+  // exact (profiles/r02g_bs_pair_ab.txt) — the paired kernel needs 100-119
+  // registers, so its doubled ILP is paid for with half the resident warps
+  const char* pe = getenv("HPAC_STREAM_PAIR");
+  const bool pair_on = pe && strcmp(pe, "1") == 0;
+  if (p.tpt % 64 == 0 && pair_on)
+    bs_stream_kernel<TECH, LEVEL, H, 2><<<nblocks, p.tpt / 2, smem, st>>>(p);
+  else
+    bs_stream_kernel<TECH, LEVEL, H, 1><<<nblocks, p.tpt, smem, st>>>(p);
+}
+
 template <int TECH, int LEVEL>
 static cudaError_t stream_launch_level(const EngineParams& p, int nblocks, size_t smem,
                                        cudaStream_t st) {
   if (TECH == HPAC_TECH_TAF) {
     switch (p.taf_h) {
 #define HPAC_S(H) \
-  case H: bs_stream_kernel<TECH, LEVEL, H><<<nblocks, p.tpt, smem, st>>>(p); break;
+  case H: stream_launch_h<TECH, LEVEL, H>(p, nblocks, smem, st); break;
       HPAC_S(1) HPAC_S(2) HPAC_S(3) HPAC_S(4) HPAC_S(5) HPAC_S(6) HPAC_S(7) HPAC_S(8)
 #undef HPAC_S
       default: return cudaErrorInvalidValue;
     }
   } else {
-    bs_stream_kernel<TECH, LEVEL, 0><<<nblocks, p.tpt, smem, st>>>(p);
+    stream_launch_h<TECH, LEVEL, 0>(p, nblocks, smem, st);
   }
   return cudaGetLastError();
 }

@@ -11,6 +11,7 @@
 #include <random>
 #include <vector>
 
+#include "apps.cuh"
 #include "hpac_device.cuh"
 #include "hpac_offload.h"
 
@@ -270,4 +271,44 @@ HPAC_API int hpac_make_blobs(int64_t n, int32_t dims, int32_t k, uint64_t seed,
       out[(size_t)i * dims + d] = centers[(size_t)c * dims + d] + noise(rng);
   }
   return HPAC_OK;
+}
+
+// ---- diagnostics: fastmath vs libdevice (tests/test_gpu_fastmath.py) ----
+namespace hpac {
+__global__ void fm_eval_kernel(int kind, const double* __restrict__ x, double* __restrict__ y,
+                               int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    switch (kind) {
+      case HPAC_FM_EXP: v = fm::exp(x[i]); break;
+      case HPAC_FM_LOG: v = fm::log(x[i]); break;
+      case HPAC_FM_ERFC: v = fm::erfc(x[i]); break;
+      case HPAC_FM_BS: {
+        const double* o = x + i * 5;
+        if (!bs_call(o[0], o[1], o[2], o[3], o[4], v)) v = NAN;
+        break;
+      }
+      case HPAC_FM_LIBDEVICE_EXP: v = ::exp(x[i]); break;
+      case HPAC_FM_LIBDEVICE_LOG: v = ::log(x[i]); break;
+      case HPAC_FM_LIBDEVICE_ERFC: v = ::erfc(x[i]); break;
+      case HPAC_FM_LIBDEVICE_BS: {
+        const double* o = x + i * 5;
+        v = bs_call_libdevice(o[0], o[1], o[2], o[3], o[4]);
+        break;
+      }
+    }
+    y[i] = v;
+  }
+}
+}  // namespace hpac
+
+HPAC_API int hpac_fm_eval(int32_t kind, const double* x, double* y, int64_t n, void* stream) {
+  if (kind < HPAC_FM_EXP || kind > HPAC_FM_LIBDEVICE_BS || n < 0 || (n > 0 && (!x || !y)))
+    return HPAC_ERR_CONFIG;
+  if (n == 0) return HPAC_OK;
+  const int64_t blocks = (n + 255) / 256;
+  hpac::fm_eval_kernel<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0,
+                         (cudaStream_t)stream>>>(kind, x, y, n);
+  return cudaGetLastError() == cudaSuccess ? HPAC_OK : HPAC_ERR_CUDA;
 }

@@ -61,6 +61,23 @@ __device__ __forceinline__ bool perfo_should_skip(int kind, int modulus, int per
   return false;
 }
 
+// The same with 32-bit step keys (streaming engines: steps < 2^31); the
+// 64-bit modulo of the general form is a ~60-instruction subroutine.
+__device__ __forceinline__ bool perfo_should_skip32(int kind, int modulus, int percent,
+                                                    uint64_t seed, int key, int trip,
+                                                    int64_t tid) {
+  switch (kind) {
+    case HPAC_PERFO_SMALL:
+    case HPAC_PERFO_HERDED_SMALL: return (unsigned)key % (unsigned)modulus == (unsigned)(modulus - 1);
+    case HPAC_PERFO_LARGE:
+    case HPAC_PERFO_HERDED_LARGE: return (unsigned)key % (unsigned)modulus != 0u;
+    case HPAC_PERFO_INI: return key < (int)(((int64_t)percent * trip) / 100);
+    case HPAC_PERFO_FINI: return key >= trip - (int)(((int64_t)percent * trip) / 100);
+    case HPAC_PERFO_RANDOM: return random_skip(seed, tid, key, percent);
+  }
+  return false;
+}
+
 // Number of valid grid-stride steps of `owner` (engine.hpp:178-185).
 __device__ __forceinline__ int64_t trip_count(int64_t owner, int64_t stride, int64_t n,
                                               int64_t steps) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <limits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +26,9 @@ cudaError_t engine_thread_launch(const EngineParams& p, int nblocks, size_t smem
 bool engine_stream_eligible(const EngineParams& p);
 size_t engine_stream_smem(const EngineParams& p);
 cudaError_t engine_stream_launch(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st);
+bool engine_bs_iact_eligible(const EngineParams& p);
+size_t engine_bs_iact_smem(EngineParams& p);
+cudaError_t engine_bs_iact_launch(const EngineParams& p, int nblocks, size_t smem, cudaStream_t st);
 size_t engine_team_seq_smem(EngineParams& p, int block);
 cudaError_t engine_team_seq_launch(const EngineParams& p, int team_end, int block, size_t smem,
                                    cudaStream_t st);
@@ -78,6 +82,23 @@ struct Scratch {
 thread_local Scratch g_scratch;
 // set by the zero-copy host entry around its launch: generic per-thread engine
 thread_local bool g_force_thread_engine = false;
+
+// Largest double x with sqrt_rn(x) <= t: sqrt is correctly rounded and
+// monotone, so sqrt_rn(ssq) <= t  <=>  ssq <= x (the iACT hit test of
+// iact.hpp:60-70 without the square root).
+static double sqrt_threshold_square(double t) {
+  if (!(t >= 0.0)) return -1.0;
+  if (std::isinf(t)) return t;
+  double x = t * t;
+  if (std::isinf(x)) x = std::numeric_limits<double>::max();
+  while (x > 0.0 && std::sqrt(x) > t) x = std::nextafter(x, 0.0);
+  for (;;) {
+    const double y = std::nextafter(x, std::numeric_limits<double>::infinity());
+    if (std::isinf(y) || std::sqrt(y) > t) break;
+    x = y;
+  }
+  return x;
+}
 
 void scratch_release() {
   for (ScratchSlot& s : g_scratch.slot) {
@@ -361,6 +382,7 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
     p.tsize = spec->iact_table_size;
     p.tpw = tpw;
     p.iact_thr = spec->iact_threshold;
+    p.iact_thr2 = sqrt_threshold_square(spec->iact_threshold);
     p.perfo_kind = spec->perfo_kind;
     p.perfo_mod = spec->perfo_modulus;
     p.perfo_pct = spec->perfo_skip_percent;
@@ -456,6 +478,12 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
       pr.kind = 3;
       pr.smem = engine_stream_smem(p);
     }
+    // iACT on Blackscholes: decide-then-price engine (engine_bs_iact.cu)
+    if (engine_bs_iact_eligible(p) && !(force && strcmp(force, "thread") == 0) &&
+        !g_force_thread_engine) {
+      pr.kind = 4;
+      pr.smem = engine_bs_iact_smem(p);
+    }
   } else {
     if (r.app == HPAC_APP_KMEANS)
       return fail(err, el, HPAC_ERR_UNSUPPORTED, "K-Means region runs under per-thread mapping");
@@ -487,6 +515,7 @@ cudaError_t launch_prepared(const Prepared& pr, cudaStream_t st) {
     case 1: return engine_team_seq_launch(pr.p, pr.team_end, pr.block, pr.smem, st);
     case 2: return binomial_team_launch(pr.p, pr.nblocks, pr.smem, st);
     case 3: return engine_stream_launch(pr.p, pr.nblocks, pr.smem, st);
+    case 4: return engine_bs_iact_launch(pr.p, pr.nblocks, pr.smem, st);
   }
   return cudaErrorInvalidValue;
 }

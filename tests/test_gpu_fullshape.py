@@ -106,6 +106,35 @@ def test_c2_binomial_headline_shape():
 
 # ---------------------------------------------------------------- C1
 
+@pytest.mark.parametrize("level", ["thread", "warp", "team"])
+def test_c1_blackscholes_iact_full_shape(level):
+    """memo(in:2:0.5) on the C1 grid through the decide-then-price engine
+    (engine_bs_iact.cu): the reference engine replays the GPU's exact prices;
+    stats, paths and approximated outputs must match bit for bit."""
+    n = 1 << 22
+    opts = E.make_bs_portfolio(n, 42)
+    grid, mapping = E.resolve_grid("blackscholes", n, items_per_thread=16)
+    spec = E.iact(2, 0.5, level=level)
+    d = dev(opts)
+    exact = torch.zeros(n, dtype=torch.float64, device="cuda")
+    E.run_region(grid, n, mapping, E.blackscholes_region(d, exact), None)
+    out = torch.zeros(n, dtype=torch.float64, device="cuda")
+    paths = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    lr = E.run_region(grid, n, mapping, E.blackscholes_region(d, out), spec, paths=paths)
+    ex = exact.cpu().numpy()
+    run, who = _runner()
+    r_out = np.zeros(n)
+    r_paths = np.zeros(n, np.uint8)
+    rc, st, msg = run(grid, n, mapping, E.table_region(opts, ex.reshape(n, 1), r_out),
+                      E.iact(2, 0.5, level=level), r_paths)
+    assert rc == 0, msg
+    _check_stats(lr.stats, st, who)
+    assert np.array_equal(paths.cpu().numpy(), r_paths)
+    assert np.array_equal(out.cpu().numpy(), r_out)
+    assert st.approx_invocations > 0.4 * n
+
+
+
 def test_c1_blackscholes_taf_full_shape():
     n = 1 << 22
     opts = E.make_bs_portfolio(n, 42)

@@ -1,5 +1,5 @@
-"""The streaming per-thread engine (csrc/engine_stream.cu: bulk-TMA staged
-input tiles) against the generic per-thread engine (HPAC_ENGINE=thread) and
+"""The streaming per-thread engines (csrc/engine_stream.cu: bulk-TMA staged
+input tiles; csrc/engine_bs_iact.cu: iACT decide-then-price) against the generic per-thread engine (HPAC_ENGINE=thread) and
 the oracle, on ragged shapes the C1 grid never exercises: partial last
 tiles (per-thread fallback loads), logical warps narrower than 32, teams of
 32..256 threads, every decision level, TAF and perforation."""
@@ -58,6 +58,13 @@ SPECS = [
     lambda: E.taf(5, 2, 0.1, "warp"),
     lambda: E.taf(5, 8, 0.5, "team"),
     lambda: E.taf(2, 1, 1.0, "warp"),
+    # iACT: the decide-then-price engine (engine_bs_iact.cu)
+    lambda: E.iact(2, 0.5),
+    lambda: E.iact(4, 0.3, 2, "warp"),
+    lambda: E.iact(3, 0.5, 1, "team"),
+    lambda: E.iact(8, 0.2),
+    lambda: E.iact(1, float("inf"), 1, "warp"),
+    lambda: E.iact(4, 0.0, None, "team"),
 ]
 
 
@@ -68,7 +75,15 @@ def test_stream_engine_equals_generic_engine(shape, si):
     opts = E.make_bs_portfolio(n, 11)
     d_opts = dev(opts)
     grid = E.GridConfig(teams, tpt, ws, ipt)
-    a = _run(grid, n, d_opts, SPECS[si])
+    try:
+        a = _run(grid, n, d_opts, SPECS[si])
+    except E.ArenaOverflowError as e:
+        # the reference's arena charge (bind_technique) applies to both engines
+        with pytest.raises(E.ArenaOverflowError) as f:
+            _run(grid, n, d_opts, SPECS[si], engine="thread")
+        assert (e.required_bytes, e.available_bytes) == (f.value.required_bytes,
+                                                         f.value.available_bytes)
+        return
     b = _run(grid, n, d_opts, SPECS[si], engine="thread")
     for f in STAT_FIELDS:
         assert a[0].stats[f] == b[0].stats[f], f
@@ -76,7 +91,7 @@ def test_stream_engine_equals_generic_engine(shape, si):
     assert np.array_equal(a[2], b[2])
 
 
-@pytest.mark.parametrize("si", [1, 2, 3, 6, 8])
+@pytest.mark.parametrize("si", [1, 2, 3, 6, 8, 13, 14, 15])
 def test_stream_engine_vs_oracle_ragged(si):
     teams, tpt, ws, ipt, n = SHAPES[0]
     opts = E.make_bs_portfolio(n, 5)
@@ -106,3 +121,42 @@ def test_stream_engine_misaligned_input_falls_back():
     a = _run(grid, n, d_view, lambda: E.taf(5, 1, 0.5))
     b = _run(grid, n, dev(opts[:n]), lambda: E.taf(5, 1, 0.5))
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_iact_engine_misaligned_input_falls_back():
+    n = 32 * 64 * 4
+    opts = E.make_bs_portfolio(n + 1, 3)
+    buf = torch.from_numpy(np.concatenate([[0.0], opts.reshape(-1)])).cuda()
+    d_view = buf[1:].view(n + 1, 5)[:n]
+    grid = E.GridConfig(32, 64, 32, 4)
+    a = _run(grid, n, d_view, lambda: E.iact(2, 0.5))
+    b = _run(grid, n, dev(opts[:n]), lambda: E.iact(2, 0.5))
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_iact_engine_without_output_buffer():
+    # out = NULL: decisions and stats only (the hit copies have no target)
+    n = 16 * 64 * 8
+    opts = E.make_bs_portfolio(n, 4)
+    grid = E.GridConfig(16, 64, 32, 8)
+    lr = E.run_region(grid, n, 0, E.blackscholes_region(dev(opts), None), E.iact(2, 0.5))
+    ref = _run(grid, n, dev(opts), lambda: E.iact(2, 0.5), engine="thread")[0]
+    for f in STAT_FIELDS:
+        assert lr.stats[f] == ref.stats[f], f
+
+
+@pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[3], SHAPES[4]])
+@pytest.mark.parametrize("si", [0, 1, 2, 3, 6, 8])
+def test_paired_stream_kernel_equals_unpaired(shape, si, monkeypatch):
+    # HPAC_STREAM_PAIR=1: two logical threads per CUDA thread (opt-in variant)
+    teams, tpt, ws, ipt, n = shape
+    opts = E.make_bs_portfolio(n, 13)
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    a = _run(grid, n, d_opts, SPECS[si])
+    monkeypatch.setenv("HPAC_STREAM_PAIR", "1")
+    b = _run(grid, n, d_opts, SPECS[si])
+    for f in STAT_FIELDS:
+        assert a[0].stats[f] == b[0].stats[f], f
+    assert np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2])
