@@ -898,9 +898,9 @@ def our_arm(args, wl, emit=True):
         "approx_rate": st_apx["approx_invocations"] / max(1, st_apx["total_invocations"]),
         "divergent_fraction": st_apx["divergent_warp_steps"] / max(1, st_apx["total_warp_steps"]),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        # one region kernel per step (+ the DMMA operand kernel for K-Means)
-        "gpu_launches": args.steps * (2 if wl["benchmark"] == "kmeans"
-                                      and kmeans_uses_dmma(wl["dims"], wl["k"]) else 1),
+        # region kernels per step: one, + the DMMA operand kernel for K-Means;
+        # binomial (non-TAF) = decide + price (+ resolve for iACT)
+        "gpu_launches": args.steps * region_launches(wl),
         "clocks": clk, **extra,
     }
     if emit:
@@ -909,6 +909,16 @@ def our_arm(args, wl, emit=True):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def region_launches(wl):
+    """Kernels one run_region launch of this workload enqueues (csrc/*.cu)."""
+    if wl["benchmark"] == "kmeans" and kmeans_uses_dmma(wl["dims"], wl["k"]):
+        return 2  # kmeans_dmma_aux_kernel + engine_thread_kernel
+    if wl["benchmark"] == "binomial" and wl["spec"][0] != "taf":
+        # binomial_decide_kernel + binomial_price_kernel (+ binomial_resolve_kernel)
+        return 3 if wl["spec"][0] == "iact" else 2
+    return 1
 
 
 def kmeans_lloyd_arm(args, wl, emit=True):

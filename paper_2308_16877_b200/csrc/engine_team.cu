@@ -24,8 +24,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "apps.cuh"
+#include "fastmath.cuh"
 #include "engine.h"
 #include "hpac_device.cuh"
 
@@ -540,6 +543,260 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Segmented boundary tracking: 32/SEG American puts per warp, SEG lanes each.
+//
+// With the early-exercise prefix and the negligible out-of-the-money tail
+// cut, an option's live node range is ~80-130 nodes per level (boundary to
+// the eps*K tail; SURVEY §8a-A10 restated in DESIGN.md §4.3), i.e. ~3-4
+// nodes per lane of a whole warp, so per-level work (shuffle, exercise
+// recurrence start, loop control, boundary check) outweighed the node
+// updates. Here each option gets a SEG-lane segment of ~SEG x B nodes and
+// the per-level overhead is spread over 32/SEG times more nodes. Node values
+// are computed with the same fma/max per node as binomial_put_bt, but with
+// per-node exercise registers (bts_phase), so an option's price does not
+// depend on the warp's block size (that is, on the other options in the
+// warp). Per option the nodes live in a window [lo, lo + WIN) of this warp's
+// shared memory, re-based to the next phase's bound at the end of every
+// phase. Options whose live range outgrows SEG * BMAX, whose boundary check
+// fails, or whose price is too small for the tail cut return false and are
+// priced by the whole-warp path (also a pure function of the option).
+constexpr int kSegPhase = 32;   // levels per phase (= binomial_put_bt)
+constexpr int kSegMargin = 8;   // nodes kept below the measured boundary
+
+// per-segment block bound: SEG * BMAX = 160 live nodes; chunk C: 4 nodes
+// per exercise register for SEG 8 (blocks 4..20), 2 for SEG 16 (blocks 2..10)
+#ifndef HPAC_SEG_C
+#define HPAC_SEG_C 0  // 0: by segment width
+#endif
+template <int SEG>
+struct SegWin {
+  static constexpr int C = HPAC_SEG_C > 0 ? HPAC_SEG_C : (SEG <= 8 ? 4 : 2);
+  static constexpr int BMAX = 160 / SEG;
+  static constexpr int WIN = 160 + 32;  // live range + bound drift
+};
+
+// One phase (<= kSegPhase levels) on B-node register blocks, B a multiple
+// of the chunk C (2 or 4). The exercise values come from one register per
+// C-node chunk starting at j (j - lo a multiple of C): x_j(L) = K - S*up^(2j-L)
+// is anchored exactly (exp) at the phase's first level and stepped down a
+// level per iteration (x' = fma(x, up, c1)); inside the chunk x_{j+1} =
+// fma(x_j, up^2, c2), x_{j+2} = fma(x_j, up^4, c4), x_{j+3} = fma(x_{j+1},
+// up^4, c4). All of it depends on (lo, j, L) only, so a node's value never
+// depends on how the range is cut into lane blocks: the block size can follow
+// the widest option of the warp while every option's price stays a pure
+// function of the option.
+template <int C>
+__device__ __forceinline__ double chunk_x(double a, int r, const LatParams& q) {
+  if (r == 0) return a;
+  const double b = fma(a, q.up2, q.c2);
+  if (r == 1) return b;
+  if (r == 2) return fma(a, q.up4, q.c4);
+  return fma(b, q.up4, q.c4);
+}
+
+template <int B, int BMAX, int SEG, int C>
+__device__ __forceinline__ void bts_phase(double (&v)[BMAX], double (&xa)[BMAX / C], int& L,
+                                          int lo, const LatParams& q, int sub, const double* w,
+                                          bool check, bool& ok, int& cnt_out, int& js_out,
+                                          int top, double eps_k) {
+  static_assert(B % C == 0, "whole chunks");
+  const int base = lo + sub * B;
+#pragma unroll
+  for (int i = 0; i < B; ++i) v[i] = base + i <= top ? w[sub * B + i] : 0.0;
+#pragma unroll
+  for (int k = 0; k < B / C; ++k)
+    xa[k] = q.K - q.S * fm::exp((double)(2 * (base + C * k) - L) * q.lnu);
+  int L_last = L;
+  for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
+    if (done > 0) {
+#pragma unroll
+      for (int k = 0; k < B / C; ++k) xa[k] = fma(xa[k], q.up, q.c1);
+    }
+    double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+    if (sub == SEG - 1) vr = 0.0;  // the segment's top node: right neighbour 0
+#pragma unroll
+    for (int k = 0; k < B / C; ++k) {
+      double xb = 0.0;
+#pragma unroll
+      for (int r = 0; r < C; ++r) {
+        const int i = k * C + r;
+        const double right = (i + 1 < B) ? v[i + 1] : vr;
+        const double cont = fma(q.pd, right, q.qd * v[i]);
+        double x;
+        if (r == 0) x = xa[k];
+        else if (r == 1) x = xb = fma(xa[k], q.up2, q.c2);
+        else if (r == 2) x = fma(xa[k], q.up4, q.c4);
+        else x = fma(xb, q.up4, q.c4);
+        v[i] = ((i & 1) == 0 || !HPAC_LAT_FPMAX_ODD) ? max_nonneg(cont, x) : max_fp(cont, x);
+      }
+    }
+    ok = ok && !(check && v[0] != xa[0]);  // node lo stays exercised (sub 0)
+    L_last = L;
+    --L;
+  }
+  int cnt = 0, js = -1;
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const double x = chunk_x<C>(xa[i / C], i % C, q);
+    if (base + i <= L_last && v[i] == x) ++cnt;
+    if (base + i <= L_last && base + i <= top && v[i] > eps_k) js = base + i;
+  }
+  cnt_out = cnt;
+  js_out = js;
+}
+
+template <int SEG>
+__device__ __forceinline__ int seg_sum(int x) {
+#pragma unroll
+  for (int o = SEG >> 1; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+template <int SEG>
+__device__ __forceinline__ int seg_max(int x) {
+#pragma unroll
+  for (int o = SEG >> 1; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// CRR parameters of binomial_price (bench/binomial.hpp:16-32); false where
+// the reference throws.
+__device__ __forceinline__ bool lat_params(double spot, double strike, double rate, double vol,
+                                           double mat, int N, bool put, LatParams& q) {
+  if (!(spot > 0) || !(strike > 0) || !(mat > 0) || !(vol > 0) || N < 1) return false;
+  const double dt = mat / N;
+  const double lnu = vol * sqrt(dt);
+  const double up = exp(lnu);
+  const double down = 1.0 / up;
+  const double growth = exp(rate * dt);
+  const double pu = (growth - down) / (up - down);
+  if (!(pu > 0.0) || !(pu < 1.0)) return false;
+  const double disc = 1.0 / growth;
+  q.K = strike;
+  q.pd = disc * pu;
+  q.qd = disc * (1.0 - pu);
+  q.up = up;
+  q.up2 = up * up;
+  q.lnu = lnu;
+  q.S = spot;
+  lat_offsets(q, put);
+  return true;
+}
+
+// All 32 lanes call, converged; segment g = lane / SEG prices option `o`
+// (its own lanes' copy; `has` false = idle segment) in window w_g. Returns
+// the segment's success; price valid on every lane of a successful segment.
+template <int SEG, int BMAX>
+__device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* w, double& price,
+                                 unsigned long long& nodes) {
+  constexpr int WIN = SegWin<SEG>::WIN;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % SEG;
+  LatParams q;
+  bool alive = has && lat_params(o[0], o[1], o[2], o[3], o[4], N, true, q);
+  if (!alive) {  // keep the idle segment's arithmetic finite
+    q.K = q.S = 1.0;
+    q.pd = q.qd = 0.5;
+    q.up = q.up2 = q.up4 = 1.0;
+    q.lnu = 0.0;
+    q.c1 = q.c2 = q.c4 = 0.0;
+  }
+  bool success = alive;
+  const double spot = q.S, strike = q.K;
+  int lo = alive ? (int)floor(((double)(N - 1 - kSegPhase) + log(strike / spot) / q.lnu) * 0.5) - 48
+                 : 0;
+  lo = max(0, min(lo, N / 2));
+  // leaves within the window; the highest in-the-money leaf must be inside
+  int jk = -1;
+  for (int j = lo + sub; j < lo + WIN; j += SEG) {
+    double x = 0.0;
+    if (j <= N) {
+      x = strike - spot * exp((double)(2 * j - N) * q.lnu);
+      if (x > 0.0) jk = j;
+    }
+    w[j - lo] = x < 0.0 ? 0.0 : x;
+  }
+  jk = seg_max<SEG>(jk);
+  price = 0.0;
+  if (alive && jk >= lo + WIN - 1 && lo + WIN - 1 <= N) success = alive = false;
+  if (alive && jk < lo) {
+    alive = false;
+    success = jk < 0 && lo == 0;  // every node exactly 0 (binomial_put_bt)
+  }
+  unsigned long long my_nodes = 0;
+  int hi = jk;
+  const double eps_k = kBtTailEps * strike;
+  constexpr int C = SegWin<SEG>::C;
+  double v[BMAX], xa[BMAX / C];
+  int L = N - 1;
+  __syncwarp();
+  while (L >= 0) {
+    const int top = hi + 1;
+    const int live = min(L, hi) + 2 - lo;
+    if (alive && (live > SEG * BMAX || live < 1)) success = alive = false;
+    const int need = alive ? (live + SEG - 1) / SEG : 0;
+    const int bw = __reduce_max_sync(0xffffffffu, need);
+    if (bw == 0) break;
+    if (alive && sub == 0) {
+      const int lv = min(L + 1, kSegPhase);
+      for (int t = 0; t < lv; ++t) my_nodes += (unsigned long long)max(0, min(L - t, hi) + 1 - lo);
+    }
+    bool ok = true;
+    int cnt = 0, js = -1;
+    const bool check = lo > 0;
+    int Bsel = 0;
+#define HPAC_BTS(b, bn)                                                                      \
+  if (bw > (bn)) {                                                                           \
+    Bsel = (b);                                                                              \
+    bts_phase<(b), BMAX, SEG, C>(v, xa, L, lo, q, sub, w, check, ok, cnt, js, top, eps_k);   \
+  } else
+    if constexpr (C == 4) {
+      HPAC_BTS(20, 16) HPAC_BTS(16, 12) HPAC_BTS(12, 8) HPAC_BTS(8, 4) HPAC_BTS(4, 0) {}
+    } else if constexpr (BMAX == 20) {
+      HPAC_BTS(20, 18) HPAC_BTS(18, 16) HPAC_BTS(16, 14) HPAC_BTS(14, 12) HPAC_BTS(12, 10)
+      HPAC_BTS(10, 8) HPAC_BTS(8, 6) HPAC_BTS(6, 4) HPAC_BTS(4, 2) HPAC_BTS(2, 0) {}
+    } else {
+      HPAC_BTS(10, 8) HPAC_BTS(8, 6) HPAC_BTS(6, 4) HPAC_BTS(4, 2) HPAC_BTS(2, 0) {}
+    }
+#undef HPAC_BTS
+    const int nex = seg_sum<SEG>(cnt);
+    const int jsig = seg_max<SEG>(js);
+    const bool ok0 = __shfl_sync(0xffffffffu, ok ? 1 : 0, lane - sub) != 0;
+    if (alive && !ok0) success = alive = false;
+    // next bound (binomial_put_bt): measured boundary minus margin and half
+    // a phase of drift; full range near the root; the tail cap follows the
+    // last significant node
+    const int hi_new = max(min(hi, jsig), lo);
+    int lo_new = lo + nex - kSegMargin - kSegPhase / 2;
+    if (L < 3 * kSegPhase) lo_new = 0;
+    lo_new = max(0, min(lo_new, (L + 1) / 2));
+    if (L < 0) lo_new = lo;  // done: node 0 stays at window index 0 (lo == 0)
+    if (alive && hi_new + 1 - lo_new + 1 > WIN) success = alive = false;
+    __syncwarp();
+    if (alive) {
+      // write back re-based to lo_new (nodes below it are exercised: dropped)
+      const int base = lo + sub * Bsel;
+#pragma unroll
+      for (int i = 0; i < BMAX; ++i) {
+        const int j = base + i;
+        if (i < Bsel && j <= top && j >= lo_new && j - lo_new < WIN) w[j - lo_new] = v[i];
+      }
+      // nodes entering from below are exactly their exercise values (level L+1)
+      for (int j = lo_new + sub; j < lo; j += SEG)
+        w[j - lo_new] = strike - spot * exp((double)(2 * j - (L + 1)) * q.lnu);
+      lo = lo_new;
+      hi = hi_new;
+    }
+    __syncwarp();
+  }
+  if (success && alive) price = w[0];
+  __syncwarp();
+  // the tail cut is only valid when N*eps*K << price (binomial_warp_price)
+  if (success && alive && !(price * 1e-9 >= (double)N * kBtTailEps * strike)) success = false;
+  if (success && sub == 0) nodes += my_nodes;
+  return success;
+}
+
 // binomial_price (bench/binomial.hpp:16-50) by one warp; every lane
 // returns the price. `xch` = 32*BMAX doubles of this warp's shared memory.
 template <int BMAX, bool AM, bool PUT>
@@ -703,6 +960,11 @@ __device__ double binomial_warp_price_smem(const double* o, int N, double* buf, 
 }
 
 constexpr int kLatBmax = 33;  // register lattice up to N = 32*33 - 1 = 1055 steps
+#ifndef HPAC_BINO_SEG
+#define HPAC_BINO_SEG 8
+#endif
+constexpr int kBinoSeg = HPAC_BINO_SEG;  // lanes per American put (0 = whole warp)
+constexpr int kBinoSegW = kBinoSeg > 0 ? kBinoSeg : 32;  // (keeps the disabled path well-formed)
 constexpr int kBinoChunk = 256;
 constexpr int kBinoWarps = 2;  // = threads_per_team / 32 at the default tpt 64
 #ifndef HPAC_BINO_MIN_CTAS
@@ -764,9 +1026,23 @@ __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_
         double o[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) o[d] = p.region.in[idx * 5 + d];
-        bool ok;
-        outv = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
-                   : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok, &p.counters[kCntLatticeFallback]);
+        bool ok = true;
+        bool priced = false;
+        if constexpr (AM && PUT && kBinoSeg > 0) {
+          // the exact path's pricing function (segment 0 of the warp)
+          if (!big) {
+            unsigned long long nodes = 0;
+            double v;
+            const bool okseg = binomial_put_seg<kBinoSegW, SegWin<kBinoSegW>::BMAX>(
+                o, lane < kBinoSegW, N, xch + (lane / kBinoSegW) * SegWin<kBinoSegW>::WIN, v, nodes);
+            priced = __shfl_sync(0xffffffffu, okseg ? 1 : 0, 0) != 0;
+            outv = __shfl_sync(0xffffffffu, v, 0);
+            if (priced && lane == 0) atomicAdd(&p.counters[kCntLatticeNodes], nodes);
+          }
+        }
+        if (!priced)
+          outv = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
+                     : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok, &p.counters[kCntLatticeFallback]);
         if (!ok) err = true;
         // TafState::observe_accurate (single output)
         const int h = p.taf_h;
@@ -855,7 +1131,50 @@ __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_
     __syncthreads();
     // ---- phase 2: misses evaluated by the team's warps --------------------
     const int nm = *nmiss_s;
+    if constexpr (AM && PUT && kBinoSeg > 0) {
+      // American puts: 32/SEG options per warp (binomial_put_seg); options
+      // it declines go through the whole-warp path below, one at a time
+      if (!big) {
+        constexpr int NSEG = 32 / kBinoSegW;
+        const int g = lane / kBinoSegW;
+        for (int m0 = warp * NSEG; m0 < nm; m0 += kBinoWarps * NSEG) {
+          const int m = m0 + g;
+          const bool has = m < nm;
+          double o[5] = {100.0, 100.0, 0.05, 0.25, 1.0};
+          if (has) {
+            const int64_t idx = team + (base + miss[m]) * p.stride;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) o[d] = __ldg(p.region.in + idx * 5 + d);
+          }
+          double v;
+          unsigned long long nodes = 0;
+          const bool okseg = binomial_put_seg<kBinoSegW, SegWin<kBinoSegW>::BMAX>(
+              o, has, N, xch + g * SegWin<kBinoSegW>::WIN, v, nodes);
+          if (has && okseg && (lane % kBinoSegW) == 0) {
+            price[miss[m]] = v;
+            atomicAdd(&p.counters[kCntLatticeNodes], nodes);
+          }
+          unsigned fb = __ballot_sync(0xffffffffu, has && !okseg && (lane % kBinoSegW) == 0);
+          while (fb) {
+            const int gg = (__ffs(fb) - 1) / kBinoSegW;
+            fb &= fb - 1;
+            const int sm = miss[m0 + gg];
+            const int64_t idx = team + (base + sm) * p.stride;
+            double oo[5];
+#pragma unroll
+            for (int d = 0; d < 5; ++d) oo[d] = __ldg(p.region.in + idx * 5 + d);
+            bool ok;
+            const double vv = binomial_warp_price<kLatBmax, AM, PUT>(oo, N, xch, ok,
+                                                                     &p.counters[kCntLatticeFallback]);
+            if (!ok) err = true;
+            if (lane == 0) price[sm] = vv;
+          }
+        }
+      }
+    }
     for (int m = warp; m < nm; m += kBinoWarps) {
+      if constexpr (AM && PUT && kBinoSeg > 0)
+        if (!big) break;
       const int s = miss[m];
       const int64_t idx = team + (base + s) * p.stride;
       double o[5];
@@ -891,6 +1210,277 @@ __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_
   }
   if (threadIdx.x != 0) tot = app = wsteps = 0;
   flush_stats(p, tot, app, wsteps, (threadIdx.x == 0 && trip > 0) ? wpt : 0ull, err);
+}
+
+// ---------------------------------------------------------------------------
+// Binomial region without TAF: decide -> price -> resolve.
+//
+// Under the per-team mapping every lane of a team sees the same option, so
+// iACT (one team-shared table) and perforation decide on the
+// inputs alone, sequentially per team; the lattices are the cost, and they
+// are independent of each other. So the launch is split:
+//  1. binomial_decide_kernel: one warp per team walks the team's item stream
+//     (inputs staged 32 steps at a time), runs the table / perforation
+//     protocol on lane 0, and writes per item the producing step of a hit
+//     (iACT), appends misses to a global list, and the stats / path bits;
+//  2. binomial_price_kernel: persistent CTAs; each warp takes batches of
+//     misses from an atomic counter (32/SEG American puts per batch through
+//     binomial_put_seg, else one option per warp) and writes their prices —
+//     no team's misses wait on another team's, no tail of uneven CTAs;
+//  3. binomial_resolve_kernel: every hit copies its producer's price.
+// Exact (spec NULL) launches price every item of the team range directly.
+// ---------------------------------------------------------------------------
+struct BinoWork {
+  int* act;        // [n] producing step of a hit (>= 0), -1 priced, -2 skipped (iACT only)
+  int* miss;       // [n] items to price (iACT / perforation)
+  unsigned* ctr;   // [0] misses, [1] batch counter
+};
+
+__host__ __device__ inline int bino_decide_warp_doubles(int ts) {
+  return 160 + 5 * ts + (ts + 32 + 1) / 2;  // staged inputs, table, producing steps, miss list
+}
+
+template <int TECH>
+__global__ void __launch_bounds__(128) binomial_decide_kernel(const EngineParams p, int team_end,
+                                                              BinoWork wk) {
+  extern __shared__ __align__(16) double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = p.team_begin + (int)blockIdx.x * 4 + warp;
+  if (team >= team_end) return;  // whole warp
+  const int ts = p.tsize > 0 ? p.tsize : 1;
+  double* inb = sm + warp * bino_decide_warp_doubles(ts);  // [32][5]
+  double* tab = inb + 160;                                  // [ts][5]
+  int* src = reinterpret_cast<int*>(tab + 5 * ts);          // [ts]
+  int* ml = src + ts;                                       // [32]
+  const int64_t G = p.stride;
+  const int64_t trip = trip_count(team, G, p.n, p.steps);
+  const unsigned long long tpt = (unsigned long long)p.tpt, wpt = (unsigned long long)p.wpt;
+  unsigned long long app = 0;
+  int rr = 0, occ = 0;
+  for (int64_t b0 = 0; b0 < trip; b0 += 32) {
+    const int cnt = (int)(trip - b0 < 32 ? trip - b0 : 32);
+    if (TECH == HPAC_TECH_IACT && lane < cnt) {
+      const double* o = p.region.in + (team + (b0 + lane) * G) * 5;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) inb[lane * 5 + d] = __ldg(o + d);
+    }
+    __syncwarp();
+    int nm = 0, mbase = 0;
+    if (lane == 0) {
+      for (int s = 0; s < cnt; ++s) {
+        const int64_t step = b0 + s;
+        const int64_t item = team + step * G;
+        int a = -1;
+        if (TECH == HPAC_TECH_IACT) {
+          // one team-shared MemoTable (iact.hpp:58-145): a hit emits the
+          // slot's output, a miss is inserted at the round-robin cursor
+          int hit, near;
+          team_lookup(tab, 1, 5, 5, inb + s * 5, occ, p.iact_thr, hit, near);
+          if (hit >= 0) {
+            a = src[hit];
+          } else {
+#pragma unroll
+            for (int d = 0; d < 5; ++d) tab[rr * 5 + d] = inb[s * 5 + d];
+            src[rr] = (int)step;
+            rr = rr + 1 == p.tsize ? 0 : rr + 1;
+            occ = occ + 1 < p.tsize ? occ + 1 : p.tsize;
+          }
+          wk.act[item] = a;
+        } else if (TECH == HPAC_TECH_PERFO) {
+          if (perfo_should_skip(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, step, trip,
+                                team))
+            a = -2;
+        }
+        if (a == -1) ml[nm++] = (int)item;
+        else app += tpt;
+        if (p.paths) p.paths[item] = a != -1 ? 1 : 0;
+      }
+      if (nm) mbase = (int)atomicAdd(&wk.ctr[0], (unsigned)nm);
+    }
+    nm = __shfl_sync(0xffffffffu, nm, 0);
+    mbase = __shfl_sync(0xffffffffu, mbase, 0);
+    __syncwarp();
+    for (int k = lane; k < nm; k += 32) wk.miss[mbase + k] = ml[k];
+    __syncwarp();
+  }
+  if (lane == 0 && trip > 0) {
+    atomicAdd(&p.counters[kCntTotal], (unsigned long long)trip * tpt);
+    atomicAdd(&p.counters[kCntWarpSteps], (unsigned long long)trip * wpt);
+    atomicAdd(&p.counters[kCntResidentWarps], wpt);
+    if (app) atomicAdd(&p.counters[kCntApprox], app);
+  }
+}
+
+// exact launches: stats and (zero) path bits of every item of the range
+__global__ void binomial_exact_stats_kernel(const EngineParams p, int team_end) {
+  const int64_t G = p.stride;
+  const int nr = team_end - p.team_begin;
+  const unsigned long long tpt = (unsigned long long)p.tpt, wpt = (unsigned long long)p.wpt;
+  unsigned long long tot = 0, ws = 0, res = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += gridDim.x * blockDim.x) {
+    const int team = p.team_begin + t;
+    const int64_t trip = trip_count(team, G, p.n, p.steps);
+    tot += trip * tpt;
+    ws += trip * wpt;
+    if (trip > 0) res += wpt;
+    if (p.paths)
+      for (int64_t s = 0; s < trip; ++s) p.paths[team + s * G] = 0;
+  }
+  flush_stats(p, tot, 0ull, ws, res, false);
+}
+
+template <bool AM, bool PUT>
+__global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS)
+    binomial_price_kernel(const EngineParams p, int team_end, BinoWork wk, int use_list) {
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = p.region.binomial_steps;
+  const bool big = N + 1 > 32 * kLatBmax;
+  const int xch_per_warp = big ? 2 * (N + 2) : 32 * kLatBmax;
+  double* xch = smem + warp * xch_per_warp;
+  const int64_t G = p.stride;
+  const int nr = team_end - p.team_begin;
+  // items to price: the miss list, or every (team, step) of the range
+  const int64_t m_total = use_list ? (int64_t)*(volatile unsigned*)&wk.ctr[0] : (int64_t)nr * p.steps;
+  auto item_of = [&](int64_t m) -> int64_t {
+    if (use_list) return wk.miss[m];
+    const int64_t it = p.team_begin + m % nr + (m / nr) * G;
+    return it < p.n ? it : -1;
+  };
+  constexpr bool SEGD = AM && PUT && kBinoSeg > 0;
+  const int NSEG = SEGD && !big ? 32 / kBinoSegW : 1;
+  bool err = false;
+  for (;;) {
+    unsigned b = 0;
+    if (lane == 0) b = atomicAdd(&wk.ctr[1], 1u);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    const int64_t m0 = (int64_t)b * NSEG;
+    if (m0 >= m_total) break;
+    bool done = false;
+    if constexpr (SEGD) {
+      if (!big) {
+        done = true;
+        const int g = lane / kBinoSegW;
+        const int64_t m = m0 + g;
+        const int64_t item = m < m_total ? item_of(m) : -1;
+        const bool has = item >= 0;
+        double o[5] = {100.0, 100.0, 0.05, 0.25, 1.0};
+        if (has) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) o[d] = __ldg(p.region.in + item * 5 + d);
+        }
+        double v;
+        unsigned long long nodes = 0;
+        const bool okseg = binomial_put_seg<kBinoSegW, SegWin<kBinoSegW>::BMAX>(
+            o, has, N, xch + g * SegWin<kBinoSegW>::WIN, v, nodes);
+        if (has && okseg && (lane % kBinoSegW) == 0) {
+          if (p.region.out) p.region.out[item] = v;
+          atomicAdd(&p.counters[kCntLatticeNodes], nodes);
+        }
+        unsigned fb = __ballot_sync(0xffffffffu, has && !okseg && (lane % kBinoSegW) == 0);
+        while (fb) {
+          const int gg = (__ffs(fb) - 1) / kBinoSegW;
+          fb &= fb - 1;
+          const int64_t it = item_of(m0 + gg);
+          double oo[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) oo[d] = __ldg(p.region.in + it * 5 + d);
+          bool ok;
+          const double vv = binomial_warp_price<kLatBmax, AM, PUT>(oo, N, xch, ok,
+                                                                   &p.counters[kCntLatticeFallback]);
+          if (!ok) err = true;
+          if (lane == 0 && p.region.out) p.region.out[it] = vv;
+        }
+      }
+    }
+    if (!done) {
+      const int64_t item = item_of(m0);
+      if (item >= 0) {
+        double o[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) o[d] = __ldg(p.region.in + item * 5 + d);
+        bool ok;
+        const double v = big ? binomial_warp_price_smem<AM, PUT>(o, N, xch, ok)
+                             : binomial_warp_price<kLatBmax, AM, PUT>(o, N, xch, ok,
+                                                                      &p.counters[kCntLatticeFallback]);
+        if (!ok) err = true;
+        if (lane == 0 && p.region.out) p.region.out[item] = v;
+      }
+    }
+  }
+  const unsigned e = __ballot_sync(0xffffffffu, err);
+  if (lane == 0 && e) atomicAdd(&p.counters[kCntAppError], 1ull);
+}
+
+__global__ void binomial_resolve_kernel(const EngineParams p, int team_end, const int* act) {
+  const int64_t G = p.stride;
+  const int nr = team_end - p.team_begin;
+  const int64_t total = (int64_t)nr * p.steps;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int team = p.team_begin + (int)(k % nr);
+    const int64_t item = team + (k / nr) * G;
+    if (item >= p.n) continue;
+    const int a = act[item];
+    if (a >= 0) p.region.out[item] = p.region.out[team + (int64_t)a * G];
+  }
+}
+
+cudaMemPool_t bino_pool();
+
+template <bool AM, bool PUT>
+static cudaError_t launch_bino_pipeline(const EngineParams& p, int nblocks, cudaStream_t st) {
+  const int team_end = p.team_begin + nblocks;
+  const int N = p.region.binomial_steps;
+  const bool big = N + 1 > 32 * kLatBmax;
+  const bool iact = p.tech == HPAC_TECH_IACT, perfo = p.tech == HPAC_TECH_PERFO;
+  const size_t n = (size_t)p.n;
+  const size_t bytes = 16 + (iact ? n * sizeof(int) : 0) + ((iact || perfo) ? n * sizeof(int) : 0);
+  char* ws = nullptr;
+  cudaMemPool_t pool = bino_pool();
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ws), bytes, pool, st)
+                       : cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, st);
+  if (e != cudaSuccess) return e;
+  BinoWork wk;
+  wk.ctr = reinterpret_cast<unsigned*>(ws);
+  wk.act = iact ? reinterpret_cast<int*>(ws + 16) : nullptr;
+  wk.miss = (iact || perfo) ? reinterpret_cast<int*>(ws + 16 + (iact ? n * sizeof(int) : 0)) : nullptr;
+  if ((e = cudaMemsetAsync(ws, 0, 16, st)) != cudaSuccess) return e;
+  if (iact || perfo) {
+    const int ts = p.tsize > 0 ? p.tsize : 1;
+    const size_t dsm = 4 * (size_t)bino_decide_warp_doubles(ts) * sizeof(double);
+    auto kd = iact ? binomial_decide_kernel<HPAC_TECH_IACT> : binomial_decide_kernel<HPAC_TECH_PERFO>;
+    if (dsm > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)) != cudaSuccess)
+      return e;
+    kd<<<(nblocks + 3) / 4, 128, dsm, st>>>(p, team_end, wk);
+  } else {
+    binomial_exact_stats_kernel<<<(nblocks + 255) / 256 < 148 ? (nblocks + 255) / 256 : 148, 256, 0, st>>>(p, team_end);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // persistent pricing grid: every resident CTA slot, at most one per batch
+  auto kp = binomial_price_kernel<AM, PUT>;
+  const size_t psm = (size_t)kBinoWarps * (big ? 2 * (N + 2) : 32 * kLatBmax) * sizeof(double);
+  if (psm > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess)
+    return e;
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kBinoWarps * 32, psm)) != cudaSuccess)
+    return e;
+  const long long items = (long long)nblocks * p.steps;
+  const int nseg = (AM && PUT && kBinoSeg > 0 && !big) ? 32 / kBinoSegW : 1;
+  long long grid = (long long)(per_sm > 0 ? per_sm : 1) * sms;
+  const long long need = (items + (long long)nseg * kBinoWarps - 1) / ((long long)nseg * kBinoWarps);
+  if (grid > need) grid = need > 0 ? need : 1;
+  kp<<<(int)grid, kBinoWarps * 32, psm, st>>>(p, team_end, wk, (iact || perfo) ? 1 : 0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (iact && p.region.out) {
+    binomial_resolve_kernel<<<4 * sms, 256, 0, st>>>(p, team_end, wk.act);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaFreeAsync(ws, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -995,6 +1585,17 @@ template <int TECH>
 static cudaError_t launch_bino2(const EngineParams& p, int nblocks, size_t smem,
                                 cudaStream_t st) {
   const bool am = p.region.binomial_american != 0, put = p.region.binomial_put != 0;
+  // decide -> price -> resolve for everything but TAF (whose decisions need
+  // the prices); HPAC_BINO_PIPELINE=0 keeps the one-kernel chunked engine
+  const char* pe = getenv("HPAC_BINO_PIPELINE");
+  const int ts = p.tsize > 0 ? p.tsize : 1;
+  if (TECH != HPAC_TECH_TAF && !(pe && strcmp(pe, "0") == 0) && p.n < (1ll << 31) &&
+      4 * (size_t)bino_decide_warp_doubles(ts) * sizeof(double) <= 200 * 1024) {
+    if (am && put) return launch_bino_pipeline<true, true>(p, nblocks, st);
+    if (am && !put) return launch_bino_pipeline<true, false>(p, nblocks, st);
+    if (!am && put) return launch_bino_pipeline<false, true>(p, nblocks, st);
+    return launch_bino_pipeline<false, false>(p, nblocks, st);
+  }
   if (am && put) return launch_bino3<TECH, true, true>(p, nblocks, smem, st);
   if (am && !put) return launch_bino3<TECH, true, false>(p, nblocks, smem, st);
   if (!am && put) return launch_bino3<TECH, false, true>(p, nblocks, smem, st);

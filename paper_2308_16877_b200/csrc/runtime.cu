@@ -762,6 +762,11 @@ cudaMemPool_t host_entry_pool() {
   return pools[dev];
 }
 
+namespace hpac {
+// the binomial pipeline's per-launch workspace comes from the same retained pool
+cudaMemPool_t bino_pool() { return ::host_entry_pool(); }
+}  // namespace hpac
+
 // End-to-end entry with host buffers: H2D inputs, run, D2H outputs.
 HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
                                   const hpac_region_t* host_region, const hpac_spec_t* spec,

@@ -33,8 +33,10 @@ cap() {  # name, kernel regex, skip, bench args...   (CAPS=regex: only matching 
 # approximate kernels: the exact arm runs first (warmup+steps launches of the
 # TECH=3 kernel), so the first matching launch of the approximate kernel is
 # the warm-up of the timed arm
-cap binomial_iact 'binomial_team_kernel<.int.1' 0 --steps 1 --warmup 1
-cap binomial_exact 'binomial_team_kernel<.int.3' 0 --steps 1 --warmup 1
+# binomial (non-TAF): decide -> price -> resolve; the lattice kernel is the
+# price kernel (exact arm first: warmup+steps launches, then the iACT arm)
+cap binomial_iact 'binomial_price_kernel' 2 --steps 1 --warmup 1
+cap binomial_exact 'binomial_price_kernel' 0 --steps 1 --warmup 1
 cap bs_taf 'bs_stream_kernel<.int.0' 0 --workload blackscholes --steps 1 --warmup 1
 cap bs_exact 'bs_stream_kernel<.int.3' 0 --workload blackscholes --steps 1 --warmup 1
 cap lavamd_taf 'engine_thread_kernel<hpac::AppLavaMD, .int.0' 0 --workload lavamd --steps 1 --warmup 1
