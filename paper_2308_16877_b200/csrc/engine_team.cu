@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(128) engine_team_seq_kernel(const EngineParams
 #ifndef HPAC_LAT_FPMAX_ODD
 #define HPAC_LAT_FPMAX_ODD 1  // odd nodes compare on the FP64 pipe (balances pipes)
 #endif
+#ifndef HPAC_LAT_FPMAX_ALL
+#define HPAC_LAT_FPMAX_ALL 1  // segmented lattice: every node's max on the FP64 pipe (+8 %)
+#endif
 
 struct LatParams {
   double K;
@@ -561,8 +564,14 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
 // phase. Options whose live range outgrows SEG * BMAX, whose boundary check
 // fails, or whose price is too small for the tail cut return false and are
 // priced by the whole-warp path (also a pure function of the option).
-constexpr int kSegPhase = 32;   // levels per phase (= binomial_put_bt)
-constexpr int kSegMargin = 8;   // nodes kept below the measured boundary
+#ifndef HPAC_SEG_PHASE
+#define HPAC_SEG_PHASE 32
+#endif
+constexpr int kSegPhase = HPAC_SEG_PHASE;  // levels per phase (= binomial_put_bt)
+#ifndef HPAC_SEG_MARGIN
+#define HPAC_SEG_MARGIN 8
+#endif
+constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured boundary
 
 // per-segment block bound: SEG * BMAX = 160 live nodes; chunk C: 4 nodes
 // per exercise register for SEG 8 (blocks 4..20), 2 for SEG 16 (blocks 2..10)
@@ -628,7 +637,8 @@ __device__ __forceinline__ void bts_phase(double (&v)[BMAX], double (&xa)[BMAX /
         else if (r == 1) x = xb = fma(xa[k], q.up2, q.c2);
         else if (r == 2) x = fma(xa[k], q.up4, q.c4);
         else x = fma(xb, q.up4, q.c4);
-        v[i] = ((i & 1) == 0 || !HPAC_LAT_FPMAX_ODD) ? max_nonneg(cont, x) : max_fp(cont, x);
+        v[i] = (HPAC_LAT_FPMAX_ALL || ((i & 1) && HPAC_LAT_FPMAX_ODD)) ? max_fp(cont, x)
+                                                                       : max_nonneg(cont, x);
       }
     }
     ok = ok && !(check && v[0] != xa[0]);  // node lo stays exercised (sub 0)
