@@ -578,6 +578,10 @@ constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured bo
 #ifndef HPAC_SEG_C
 #define HPAC_SEG_C 0  // 0: by segment width
 #endif
+#ifndef HPAC_BINO_TWO_BAND
+#define HPAC_BINO_TWO_BAND 1  // in-the-money / out-of-the-money bands (bts_phase2)
+#endif
+constexpr bool kBinoTwoBand = HPAC_BINO_TWO_BAND != 0;
 template <int SEG>
 struct SegWin {
   static constexpr int C = HPAC_SEG_C > 0 ? HPAC_SEG_C : (SEG <= 8 ? 4 : 2);
@@ -604,12 +608,12 @@ __device__ __forceinline__ double chunk_x(double a, int r, const LatParams& q) {
   return fma(b, q.up4, q.c4);
 }
 
-template <int B, int BMAX, int SEG, int C>
-__device__ __forceinline__ void bts_phase(double (&v)[BMAX], double (&xa)[BMAX / C], int& L,
+template <int B, int BMAX, int SEG, int C, int RN, int XN>
+__device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int& L,
                                           int lo, const LatParams& q, int sub, const double* w,
                                           bool check, bool& ok, int& cnt_out, int& js_out,
                                           int top, double eps_k) {
-  static_assert(B % C == 0, "whole chunks");
+  static_assert(B % C == 0 && B <= RN && B / C <= XN, "whole chunks");
   const int base = lo + sub * B;
 #pragma unroll
   for (int i = 0; i < B; ++i) v[i] = base + i <= top ? w[sub * B + i] : 0.0;
@@ -652,6 +656,85 @@ __device__ __forceinline__ void bts_phase(double (&v)[BMAX], double (&xa)[BMAX /
     if (base + i <= L_last && v[i] == x) ++cnt;
     if (base + i <= L_last && base + i <= top && v[i] > eps_k) js = base + i;
   }
+  cnt_out = cnt;
+  js_out = js;
+}
+
+// Two-band phase: each lane holds BI nodes of the in-the-money band
+// [lo, lo + SEG*BI) and BO nodes of the band above it. The caller puts the
+// split above the highest node that can be in the money during the phase
+// (the strike node only moves down as L decreases), so in the upper band the
+// exercise value is negative and max(cont, x) = cont exactly (cont >= +0):
+// the upper band updates with DMUL + DFMA and no exercise chain, bit-identical
+// to the one-band phase. Right neighbours: the next lane's first node of the
+// same band; the segment's last lane takes the upper band's first node (lower
+// band) or 0 (upper band).
+template <int BI, int BO, int RN, int XN, int SEG, int C>
+__device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], int& L, int lo,
+                                           const LatParams& q, int sub, const double* w,
+                                           bool check, bool& ok, int& cnt_out, int& js_out,
+                                           int top, double eps_k) {
+  static_assert(BI % C == 0 && BI <= 8 && 8 + BO <= RN && BI / C <= XN, "block shapes");
+  double* const vi = r;      // lower band: r[0 .. BI)
+  double* const vo = r + 8;  // upper band: r[8 .. 8 + BO)
+  const int base_i = lo + sub * BI;
+  const int base_o = lo + SEG * BI + sub * BO;
+  const int seg0 = (int)(threadIdx.x & 31) - sub;
+#pragma unroll
+  for (int i = 0; i < BI; ++i) vi[i] = base_i + i <= top ? w[sub * BI + i] : 0.0;
+#pragma unroll
+  for (int i = 0; i < BO; ++i) vo[i] = base_o + i <= top ? w[SEG * BI + sub * BO + i] : 0.0;
+#pragma unroll
+  for (int k = 0; k < BI / C; ++k)
+    xa[k] = q.K - q.S * fm::exp((double)(2 * (base_i + C * k) - L) * q.lnu);
+  int L_last = L;
+  for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
+    if (done > 0) {
+#pragma unroll
+      for (int k = 0; k < BI / C; ++k) xa[k] = fma(xa[k], q.up, q.c1);
+    }
+    double ri = __shfl_down_sync(0xffffffffu, vi[0], 1);
+    double ro = __shfl_down_sync(0xffffffffu, vo[0], 1);
+    const double ro0 = __shfl_sync(0xffffffffu, vo[0], seg0);
+    if (sub == SEG - 1) {
+      ri = ro0;
+      ro = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < BI / C; ++k) {
+      double xb = 0.0;
+#pragma unroll
+      for (int r = 0; r < C; ++r) {
+        const int i = k * C + r;
+        const double right = (i + 1 < BI) ? vi[i + 1] : ri;
+        const double cont = fma(q.pd, right, q.qd * vi[i]);
+        double x;
+        if (r == 0) x = xa[k];
+        else if (r == 1) x = xb = fma(xa[k], q.up2, q.c2);
+        else if (r == 2) x = fma(xa[k], q.up4, q.c4);
+        else x = fma(xb, q.up4, q.c4);
+        vi[i] = max_fp(cont, x);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BO; ++i) {
+      const double right = (i + 1 < BO) ? vo[i + 1] : ro;
+      vo[i] = fma(q.pd, right, q.qd * vo[i]);
+    }
+    ok = ok && !(check && vi[0] != xa[0]);  // node lo stays exercised (sub 0)
+    L_last = L;
+    --L;
+  }
+  int cnt = 0, js = -1;
+#pragma unroll
+  for (int i = 0; i < BI; ++i) {
+    const double x = chunk_x<C>(xa[i / C], i % C, q);
+    if (base_i + i <= L_last && vi[i] == x) ++cnt;
+    if (base_i + i <= L_last && base_i + i <= top && vi[i] > eps_k) js = base_i + i;
+  }
+#pragma unroll
+  for (int i = 0; i < BO; ++i)
+    if (base_o + i <= L_last && base_o + i <= top && vo[i] > eps_k) js = base_o + i;
   cnt_out = cnt;
   js_out = js;
 }
@@ -737,7 +820,13 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
   int hi = jk;
   const double eps_k = kBtTailEps * strike;
   constexpr int C = SegWin<SEG>::C;
-  double v[BMAX], xa[BMAX / C];
+  // one register file for both phase shapes: one band v[0 .. B), or the
+  // lower band v[0 .. 8) and the upper band v[8 .. 24)
+  constexpr int RN = BMAX > 24 ? BMAX : 24;
+  double v[RN], xa[BMAX / C > 2 ? BMAX / C : 2];
+  // strike node offset: x_j(L) > 0  <=>  j < (L + ln(K/S)/lnu) / 2
+  const double lks = log(strike / spot) / q.lnu;
+  const bool lks_ok = alive && q.lnu > 1e-9 && isfinite(lks);
   int L = N - 1;
   __syncwarp();
   while (L >= 0) {
@@ -754,11 +843,41 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     bool ok = true;
     int cnt = 0, js = -1;
     const bool check = lo > 0;
-    int Bsel = 0;
+    int Bsel = 0, Bi2 = 0, Bo2 = 0;
+    // two-band shape: the lower band must reach past the highest node that
+    // can be in the money during this phase (strike node at level L, + 2)
+    if constexpr (SEG == 8 && C == 4 && kBinoTwoBand) {
+      int ni = 0;
+      if (alive) {
+        const int jo = (int)ceil(0.5 * ((double)L + lks)) + 1;
+        ni = lks_ok ? max(1, (jo - lo + SEG - 1) / SEG) : 1 << 20;
+        ni = (ni + 3) & ~3;  // whole 4-node chunks
+      }
+      const int bi = __reduce_max_sync(0xffffffffu, ni);
+      if (bi <= 8) {
+        int no = 0;
+        if (alive) no = max(0, (top + 1 - (lo + SEG * bi) + SEG - 1) / SEG);
+        const int bo = __reduce_max_sync(0xffffffffu, no);
+        if (bo > 0 && bo <= 16) {
+          Bi2 = bi;
+          Bo2 = bo <= 8 ? 8 : 16;
+        }
+      }
+    }
+    if (Bi2 > 0) {
+#define HPAC_BTS2(bi, bo)                                                                        \
+  if (Bi2 == (bi) && Bo2 == (bo)) {                                                              \
+    bts_phase2<bi, bo, RN, sizeof(xa) / sizeof(double), SEG, C>(v, xa, L, lo, q, sub, w, check,  \
+                                                               ok, cnt, js, top, eps_k);        \
+  } else
+      HPAC_BTS2(4, 8) HPAC_BTS2(4, 16) HPAC_BTS2(8, 8) HPAC_BTS2(8, 16) {}
+#undef HPAC_BTS2
+    } else
 #define HPAC_BTS(b, bn)                                                                      \
   if (bw > (bn)) {                                                                           \
     Bsel = (b);                                                                              \
-    bts_phase<(b), BMAX, SEG, C>(v, xa, L, lo, q, sub, w, check, ok, cnt, js, top, eps_k);   \
+    bts_phase<(b), BMAX, SEG, C, RN, sizeof(xa) / sizeof(double)>(v, xa, L, lo, q, sub, w, check, \
+                                                                  ok, cnt, js, top, eps_k);    \
   } else
     if constexpr (C == 4) {
       HPAC_BTS(20, 16) HPAC_BTS(16, 12) HPAC_BTS(12, 8) HPAC_BTS(8, 4) HPAC_BTS(4, 0) {}
@@ -785,11 +904,25 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     __syncwarp();
     if (alive) {
       // write back re-based to lo_new (nodes below it are exercised: dropped)
-      const int base = lo + sub * Bsel;
+      if (Bi2 > 0) {
+        const int bi_ = lo + sub * Bi2, bo_ = lo + SEG * Bi2 + sub * Bo2;
 #pragma unroll
-      for (int i = 0; i < BMAX; ++i) {
-        const int j = base + i;
-        if (i < Bsel && j <= top && j >= lo_new && j - lo_new < WIN) w[j - lo_new] = v[i];
+        for (int i = 0; i < 8; ++i) {
+          const int j = bi_ + i;
+          if (i < Bi2 && j <= top && j >= lo_new && j - lo_new < WIN) w[j - lo_new] = v[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = bo_ + i;
+          if (i < Bo2 && j <= top && j >= lo_new && j - lo_new < WIN) w[j - lo_new] = v[8 + i];
+        }
+      } else {
+        const int base = lo + sub * Bsel;
+#pragma unroll
+        for (int i = 0; i < BMAX; ++i) {
+          const int j = base + i;
+          if (i < Bsel && j <= top && j >= lo_new && j - lo_new < WIN) w[j - lo_new] = v[i];
+        }
       }
       // nodes entering from below are exactly their exercise values (level L+1)
       for (int j = lo_new + sub; j < lo; j += SEG)
