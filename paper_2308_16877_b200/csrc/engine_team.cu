@@ -262,6 +262,7 @@ struct LatParams {
   double pd, qd;  // disc * p, disc * (1 - p)
   double up, up2, up4, lnu, S;
   double c1, c2, c4;  // x recurrence offsets: +-K*(1 - up^m), m = 1, 2, 4
+  double rho, upq, rinv;  // segmented lattice, scaled phases: pd/qd, up/qd, 1/qd
 };
 
 __device__ __forceinline__ void lat_offsets(LatParams& q, bool put) {
@@ -617,14 +618,24 @@ __device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int
   const int base = lo + sub * B;
 #pragma unroll
   for (int i = 0; i < B; ++i) v[i] = base + i <= top ? w[sub * B + i] : 0.0;
+  // scaled phase (binomial_put_seg): after t levels the registers hold
+  // v / qd^t, so a node costs one DFMA (cont = rho*right + v) instead of a
+  // DMUL + DFMA; the exercise values are carried on the same scale
+  double sinv = q.rinv;  // 1/qd^(t+1) at level iteration t
+  double sq = 1.0;       // qd^t
 #pragma unroll
   for (int k = 0; k < B / C; ++k)
-    xa[k] = q.K - q.S * fm::exp((double)(2 * (base + C * k) - L) * q.lnu);
+    xa[k] = (q.K - q.S * fm::exp((double)(2 * (base + C * k) - L) * q.lnu)) * sinv;
   int L_last = L;
+  double c2t = q.c2 * sinv, c4t = q.c4 * sinv;
   for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
     if (done > 0) {
+      sinv *= q.rinv;
+      const double c1t = q.c1 * sinv;
 #pragma unroll
-      for (int k = 0; k < B / C; ++k) xa[k] = fma(xa[k], q.up, q.c1);
+      for (int k = 0; k < B / C; ++k) xa[k] = fma(xa[k], q.upq, c1t);
+      c2t = q.c2 * sinv;
+      c4t = q.c4 * sinv;
     }
     double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
     if (sub == SEG - 1) vr = 0.0;  // the segment's top node: right neighbour 0
@@ -635,26 +646,36 @@ __device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int
       for (int r = 0; r < C; ++r) {
         const int i = k * C + r;
         const double right = (i + 1 < B) ? v[i + 1] : vr;
-        const double cont = fma(q.pd, right, q.qd * v[i]);
+        const double cont = fma(q.rho, right, v[i]);
         double x;
         if (r == 0) x = xa[k];
-        else if (r == 1) x = xb = fma(xa[k], q.up2, q.c2);
-        else if (r == 2) x = fma(xa[k], q.up4, q.c4);
-        else x = fma(xb, q.up4, q.c4);
-        v[i] = (HPAC_LAT_FPMAX_ALL || ((i & 1) && HPAC_LAT_FPMAX_ODD)) ? max_fp(cont, x)
-                                                                       : max_nonneg(cont, x);
+        else if (r == 1) x = xb = fma(xa[k], q.up2, c2t);
+        else if (r == 2) x = fma(xa[k], q.up4, c4t);
+        else x = fma(xb, q.up4, c4t);
+        v[i] = max_fp(cont, x);
       }
     }
     ok = ok && !(check && v[0] != xa[0]);  // node lo stays exercised (sub 0)
+    sq *= q.qd;
     L_last = L;
     --L;
   }
   int cnt = 0, js = -1;
 #pragma unroll
-  for (int i = 0; i < B; ++i) {
-    const double x = chunk_x<C>(xa[i / C], i % C, q);
-    if (base + i <= L_last && v[i] == x) ++cnt;
-    if (base + i <= L_last && base + i <= top && v[i] > eps_k) js = base + i;
+  for (int k = 0; k < B / C; ++k) {
+    double xb = 0.0;
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      const int i = k * C + r;
+      double x;
+      if (r == 0) x = xa[k];
+      else if (r == 1) x = xb = fma(xa[k], q.up2, c2t);
+      else if (r == 2) x = fma(xa[k], q.up4, c4t);
+      else x = fma(xb, q.up4, c4t);
+      if (base + i <= L_last && v[i] == x) ++cnt;
+      v[i] *= sq;  // back to prices
+      if (base + i <= L_last && base + i <= top && v[i] > eps_k) js = base + i;
+    }
   }
   cnt_out = cnt;
   js_out = js;
@@ -684,14 +705,20 @@ __device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], in
   for (int i = 0; i < BI; ++i) vi[i] = base_i + i <= top ? w[sub * BI + i] : 0.0;
 #pragma unroll
   for (int i = 0; i < BO; ++i) vo[i] = base_o + i <= top ? w[SEG * BI + sub * BO + i] : 0.0;
+  double sinv = q.rinv, sq = 1.0;  // scaled phase, as bts_phase
 #pragma unroll
   for (int k = 0; k < BI / C; ++k)
-    xa[k] = q.K - q.S * fm::exp((double)(2 * (base_i + C * k) - L) * q.lnu);
+    xa[k] = (q.K - q.S * fm::exp((double)(2 * (base_i + C * k) - L) * q.lnu)) * sinv;
+  double c2t = q.c2 * sinv, c4t = q.c4 * sinv;
   int L_last = L;
   for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
     if (done > 0) {
+      sinv *= q.rinv;
+      const double c1t = q.c1 * sinv;
 #pragma unroll
-      for (int k = 0; k < BI / C; ++k) xa[k] = fma(xa[k], q.up, q.c1);
+      for (int k = 0; k < BI / C; ++k) xa[k] = fma(xa[k], q.upq, c1t);
+      c2t = q.c2 * sinv;
+      c4t = q.c4 * sinv;
     }
     double ri = __shfl_down_sync(0xffffffffu, vi[0], 1);
     double ro = __shfl_down_sync(0xffffffffu, vo[0], 1);
@@ -707,34 +734,47 @@ __device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], in
       for (int r = 0; r < C; ++r) {
         const int i = k * C + r;
         const double right = (i + 1 < BI) ? vi[i + 1] : ri;
-        const double cont = fma(q.pd, right, q.qd * vi[i]);
+        const double cont = fma(q.rho, right, vi[i]);
         double x;
         if (r == 0) x = xa[k];
-        else if (r == 1) x = xb = fma(xa[k], q.up2, q.c2);
-        else if (r == 2) x = fma(xa[k], q.up4, q.c4);
-        else x = fma(xb, q.up4, q.c4);
+        else if (r == 1) x = xb = fma(xa[k], q.up2, c2t);
+        else if (r == 2) x = fma(xa[k], q.up4, c4t);
+        else x = fma(xb, q.up4, c4t);
         vi[i] = max_fp(cont, x);
       }
     }
 #pragma unroll
     for (int i = 0; i < BO; ++i) {
       const double right = (i + 1 < BO) ? vo[i + 1] : ro;
-      vo[i] = fma(q.pd, right, q.qd * vo[i]);
+      vo[i] = fma(q.rho, right, vo[i]);
     }
     ok = ok && !(check && vi[0] != xa[0]);  // node lo stays exercised (sub 0)
+    sq *= q.qd;
     L_last = L;
     --L;
   }
   int cnt = 0, js = -1;
 #pragma unroll
-  for (int i = 0; i < BI; ++i) {
-    const double x = chunk_x<C>(xa[i / C], i % C, q);
-    if (base_i + i <= L_last && vi[i] == x) ++cnt;
-    if (base_i + i <= L_last && base_i + i <= top && vi[i] > eps_k) js = base_i + i;
+  for (int k = 0; k < BI / C; ++k) {
+    double xb = 0.0;
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      const int i = k * C + r;
+      double x;
+      if (r == 0) x = xa[k];
+      else if (r == 1) x = xb = fma(xa[k], q.up2, c2t);
+      else if (r == 2) x = fma(xa[k], q.up4, c4t);
+      else x = fma(xb, q.up4, c4t);
+      if (base_i + i <= L_last && vi[i] == x) ++cnt;
+      vi[i] *= sq;
+      if (base_i + i <= L_last && base_i + i <= top && vi[i] > eps_k) js = base_i + i;
+    }
   }
 #pragma unroll
-  for (int i = 0; i < BO; ++i)
+  for (int i = 0; i < BO; ++i) {
+    vo[i] *= sq;
     if (base_o + i <= L_last && base_o + i <= top && vo[i] > eps_k) js = base_o + i;
+  }
   cnt_out = cnt;
   js_out = js;
 }
@@ -773,6 +813,9 @@ __device__ __forceinline__ bool lat_params(double spot, double strike, double ra
   q.lnu = lnu;
   q.S = spot;
   lat_offsets(q, put);
+  q.rho = q.pd / q.qd;
+  q.upq = up / q.qd;
+  q.rinv = 1.0 / q.qd;
   return true;
 }
 
@@ -786,13 +829,16 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
   const int lane = threadIdx.x & 31;
   const int sub = lane % SEG;
   LatParams q;
-  bool alive = has && lat_params(o[0], o[1], o[2], o[3], o[4], N, true, q);
+  // scaled phases keep v / qd^32 in range: qd >= 1e-6 (else the whole-warp path)
+  bool alive = has && lat_params(o[0], o[1], o[2], o[3], o[4], N, true, q) && q.qd >= 1e-6;
   if (!alive) {  // keep the idle segment's arithmetic finite
     q.K = q.S = 1.0;
     q.pd = q.qd = 0.5;
     q.up = q.up2 = q.up4 = 1.0;
     q.lnu = 0.0;
     q.c1 = q.c2 = q.c4 = 0.0;
+    q.rho = 1.0;
+    q.upq = q.rinv = 2.0;
   }
   bool success = alive;
   const double spot = q.S, strike = q.K;
@@ -1472,8 +1518,11 @@ __global__ void binomial_exact_stats_kernel(const EngineParams p, int team_end) 
   flush_stats(p, tot, 0ull, ws, res, false);
 }
 
+#ifndef HPAC_BINO_PRICE_MIN_CTAS
+#define HPAC_BINO_PRICE_MIN_CTAS 7  // 146 registers (8: 128 with spills, 0.5-1 % slower)
+#endif
 template <bool AM, bool PUT>
-__global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS)
+__global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_PRICE_MIN_CTAS)
     binomial_price_kernel(const EngineParams p, int team_end, BinoWork wk, int use_list) {
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
