@@ -570,7 +570,7 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
 #endif
 constexpr int kSegPhase = HPAC_SEG_PHASE;  // levels per phase (= binomial_put_bt)
 #ifndef HPAC_SEG_MARGIN
-#define HPAC_SEG_MARGIN 8
+#define HPAC_SEG_MARGIN 5  // 2 falls off a cliff (check failures -> whole-warp path), 3 is the fastest
 #endif
 constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured boundary
 
