@@ -1519,7 +1519,7 @@ __global__ void binomial_exact_stats_kernel(const EngineParams p, int team_end) 
 }
 
 #ifndef HPAC_BINO_PRICE_MIN_CTAS
-#define HPAC_BINO_PRICE_MIN_CTAS 7  // 146 registers (8: 128 with spills, 0.5-1 % slower)
+#define HPAC_BINO_PRICE_MIN_CTAS 8  // 128 registers (ptxas picks 128 at 7 too; 6 = 168 registers: 4 % slower)
 #endif
 template <bool AM, bool PUT>
 __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_PRICE_MIN_CTAS)
