@@ -628,6 +628,10 @@ __device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int
     xa[k] = (q.K - q.S * fm::exp((double)(2 * (base + C * k) - L) * q.lnu)) * sinv;
   int L_last = L;
   double c2t = q.c2 * sinv, c4t = q.c4 * sinv;
+  // the right neighbour of the last node, one level ahead (as bts_phase2)
+  const bool last = sub == SEG - 1;
+  double vr = __shfl_down_sync(0xffffffffu, v[0], 1, SEG);
+  if (last) vr = 0.0;  // the segment's top node: right neighbour 0
   for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
     if (done > 0) {
       sinv *= q.rinv;
@@ -637,24 +641,27 @@ __device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int
       c2t = q.c2 * sinv;
       c4t = q.c4 * sinv;
     }
-    double vr = __shfl_down_sync(0xffffffffu, v[0], 1);
-    if (sub == SEG - 1) vr = 0.0;  // the segment's top node: right neighbour 0
+    const double v0 = max_fp(fma(q.rho, B > 1 ? v[1] : vr, v[0]), xa[0]);
+    const double nv = __shfl_down_sync(0xffffffffu, v0, 1, SEG);
 #pragma unroll
     for (int k = 0; k < B / C; ++k) {
       double xb = 0.0;
 #pragma unroll
       for (int r = 0; r < C; ++r) {
         const int i = k * C + r;
-        const double right = (i + 1 < B) ? v[i + 1] : vr;
-        const double cont = fma(q.rho, right, v[i]);
         double x;
         if (r == 0) x = xa[k];
         else if (r == 1) x = xb = fma(xa[k], q.up2, c2t);
         else if (r == 2) x = fma(xa[k], q.up4, c4t);
         else x = fma(xb, q.up4, c4t);
+        if (i == 0) continue;
+        const double right = (i + 1 < B) ? v[i + 1] : vr;
+        const double cont = fma(q.rho, right, v[i]);
         v[i] = max_fp(cont, x);
       }
     }
+    v[0] = v0;
+    vr = last ? 0.0 : nv;
     ok = ok && !(check && v[0] != xa[0]);  // node lo stays exercised (sub 0)
     sq *= q.qd;
     L_last = L;
@@ -711,6 +718,18 @@ __device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], in
     xa[k] = (q.K - q.S * fm::exp((double)(2 * (base_i + C * k) - L) * q.lnu)) * sinv;
   double c2t = q.c2 * sinv, c4t = q.c4 * sinv;
   int L_last = L;
+  // right neighbours of each band's last node, one level ahead: the shuffles
+  // for level t+1 are issued right after this level's first nodes, so their
+  // latency overlaps the rest of the level (width-SEG shuffles: no lane math)
+  const bool last = sub == SEG - 1;
+  double ri, ro;
+  {
+    const double a = __shfl_down_sync(0xffffffffu, vi[0], 1, SEG);
+    const double b = __shfl_down_sync(0xffffffffu, vo[0], 1, SEG);
+    const double c = __shfl_sync(0xffffffffu, vo[0], 0, SEG);
+    ri = last ? c : a;
+    ro = last ? 0.0 : b;
+  }
   for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
     if (done > 0) {
       sinv *= q.rinv;
@@ -720,34 +739,38 @@ __device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], in
       c2t = q.c2 * sinv;
       c4t = q.c4 * sinv;
     }
-    double ri = __shfl_down_sync(0xffffffffu, vi[0], 1);
-    double ro = __shfl_down_sync(0xffffffffu, vo[0], 1);
-    const double ro0 = __shfl_sync(0xffffffffu, vo[0], seg0);
-    if (sub == SEG - 1) {
-      ri = ro0;
-      ro = 0.0;
-    }
+    // first nodes of both bands, then the next level's neighbours
+    const double vo0 = fma(q.rho, BO > 1 ? vo[1] : ro, vo[0]);
+    const double vi0 = max_fp(fma(q.rho, BI > 1 ? vi[1] : ri, vi[0]), xa[0]);
+    const double na = __shfl_down_sync(0xffffffffu, vi0, 1, SEG);
+    const double nb = __shfl_down_sync(0xffffffffu, vo0, 1, SEG);
+    const double nc = __shfl_sync(0xffffffffu, vo0, 0, SEG);
 #pragma unroll
     for (int k = 0; k < BI / C; ++k) {
       double xb = 0.0;
 #pragma unroll
       for (int r = 0; r < C; ++r) {
         const int i = k * C + r;
-        const double right = (i + 1 < BI) ? vi[i + 1] : ri;
-        const double cont = fma(q.rho, right, vi[i]);
         double x;
         if (r == 0) x = xa[k];
         else if (r == 1) x = xb = fma(xa[k], q.up2, c2t);
         else if (r == 2) x = fma(xa[k], q.up4, c4t);
         else x = fma(xb, q.up4, c4t);
+        if (i == 0) continue;
+        const double right = (i + 1 < BI) ? vi[i + 1] : ri;
+        const double cont = fma(q.rho, right, vi[i]);
         vi[i] = max_fp(cont, x);
       }
     }
 #pragma unroll
-    for (int i = 0; i < BO; ++i) {
+    for (int i = 1; i < BO; ++i) {
       const double right = (i + 1 < BO) ? vo[i + 1] : ro;
       vo[i] = fma(q.rho, right, vo[i]);
     }
+    vi[0] = vi0;
+    vo[0] = vo0;
+    ri = last ? nc : na;
+    ro = last ? 0.0 : nb;
     ok = ok && !(check && vi[0] != xa[0]);  // node lo stays exercised (sub 0)
     sq *= q.qd;
     L_last = L;

@@ -102,3 +102,25 @@ def test_pipeline_vs_oracle_replay(monkeypatch):
         assert lr.stats[f] == getattr(st, f), f
     assert np.array_equal(g_paths, o_paths)
     assert np.array_equal(g_out, o_out)
+
+
+@pytest.mark.parametrize("steps", [256, 1024])
+def test_segmented_lattice_wide_parameter_range(steps, monkeypatch):
+    """American puts far from the C2 portfolio (vol 0.05-1.2, T 0.05-5,
+    r -0.01-0.08, moneyness 0.3-3; all valid CRR lattices): the 8-lane segmented lattice and its
+    whole-warp fallbacks stay within 1e-6 of the CPU lattice, and the exact
+    and iACT runs price every option identically."""
+    rng = np.random.default_rng(5)
+    n = 640
+    S = rng.uniform(20, 200, n)
+    opts = np.stack([S, S * np.exp(rng.uniform(np.log(0.3), np.log(3.0), n)), rng.uniform(-0.01, 0.08, n),
+                     rng.uniform(0.05, 1.2, n), rng.uniform(0.05, 5.0, n)], axis=1)
+    d = dev(opts)
+    grid = E.GridConfig(40, 64, 32, 16)
+    lr, out, _ = _run(grid, n, d, steps, lambda: None, True, monkeypatch)
+    want = oracle.binomial_prices(opts, steps)
+    rel = np.abs(out - want) / np.maximum(np.abs(want), 1e-300)
+    ok = (rel <= 1e-6) | (np.abs(out - want) <= 1e-12 * opts[:, 1])
+    assert ok.all(), (rel.max(), np.argmax(rel))
+    _, o2, p2 = _run(grid, n, d, steps, lambda: E.iact(2, 0.0, level="team"), True, monkeypatch)
+    assert np.array_equal(o2[p2 == 0], out[p2 == 0])
