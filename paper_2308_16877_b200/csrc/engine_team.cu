@@ -574,10 +574,14 @@ constexpr int kSegPhase = HPAC_SEG_PHASE;  // levels per phase (= binomial_put_b
 #endif
 constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured boundary
 
-// per-segment block bound: SEG * BMAX = 160 live nodes; chunk C: 4 nodes
-// per exercise register for SEG 8 (blocks 4..20), 2 for SEG 16 (blocks 2..10)
+// per-segment block bound: SEG * BMAX = 160 live nodes; chunk C: nodes per
+// exercise register (2: lower bands of 4/6/8 nodes per lane; one-band blocks
+// stay in steps of 4, HPAC_SEG_COARSE, for the instruction cache)
 #ifndef HPAC_SEG_C
 #define HPAC_SEG_C 0  // 0: by segment width
+#endif
+#ifndef HPAC_SEG_COARSE
+#define HPAC_SEG_COARSE 1  // one-band block sizes in steps of 4 also for 2-node chunks
 #endif
 #ifndef HPAC_BINO_TWO_BAND
 #define HPAC_BINO_TWO_BAND 1  // in-the-money / out-of-the-money bands (bts_phase2)
@@ -585,7 +589,7 @@ constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured bo
 constexpr bool kBinoTwoBand = HPAC_BINO_TWO_BAND != 0;
 template <int SEG>
 struct SegWin {
-  static constexpr int C = HPAC_SEG_C > 0 ? HPAC_SEG_C : (SEG <= 8 ? 4 : 2);
+  static constexpr int C = HPAC_SEG_C > 0 ? HPAC_SEG_C : 2;  // 4: 76.1 vs 80.6 M options/s (coarser lower band)
   static constexpr int BMAX = 160 / SEG;
   static constexpr int WIN = 160 + 32;  // live range + bound drift
 };
@@ -915,12 +919,13 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     int Bsel = 0, Bi2 = 0, Bo2 = 0;
     // two-band shape: the lower band must reach past the highest node that
     // can be in the money during this phase (strike node at level L, + 2)
-    if constexpr (SEG == 8 && C == 4 && kBinoTwoBand) {
+    if constexpr (SEG == 8 && (C == 4 || C == 2) && kBinoTwoBand) {
       int ni = 0;
       if (alive) {
         const int jo = (int)ceil(0.5 * ((double)L + lks)) + 1;
         ni = lks_ok ? max(1, (jo - lo + SEG - 1) / SEG) : 1 << 20;
-        ni = (ni + 3) & ~3;  // whole 4-node chunks
+        ni = (ni + C - 1) & ~(C - 1);  // whole chunks
+        ni = ni < 4 ? 4 : ni;
       }
       const int bi = __reduce_max_sync(0xffffffffu, ni);
       if (bi <= 8) {
@@ -939,7 +944,12 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     bts_phase2<bi, bo, RN, sizeof(xa) / sizeof(double), SEG, C>(v, xa, L, lo, q, sub, w, check,  \
                                                                ok, cnt, js, top, eps_k);        \
   } else
-      HPAC_BTS2(4, 8) HPAC_BTS2(4, 16) HPAC_BTS2(8, 8) HPAC_BTS2(8, 16) {}
+      if constexpr (C == 2) {
+        HPAC_BTS2(4, 8) HPAC_BTS2(4, 16) HPAC_BTS2(6, 8) HPAC_BTS2(6, 16) HPAC_BTS2(8, 8)
+        HPAC_BTS2(8, 16) {}
+      } else {
+        HPAC_BTS2(4, 8) HPAC_BTS2(4, 16) HPAC_BTS2(8, 8) HPAC_BTS2(8, 16) {}
+      }
 #undef HPAC_BTS2
     } else
 #define HPAC_BTS(b, bn)                                                                      \
@@ -948,7 +958,7 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     bts_phase<(b), BMAX, SEG, C, RN, sizeof(xa) / sizeof(double)>(v, xa, L, lo, q, sub, w, check, \
                                                                   ok, cnt, js, top, eps_k);    \
   } else
-    if constexpr (C == 4) {
+    if constexpr (C == 4 || (C == 2 && BMAX == 20 && HPAC_SEG_COARSE)) {
       HPAC_BTS(20, 16) HPAC_BTS(16, 12) HPAC_BTS(12, 8) HPAC_BTS(8, 4) HPAC_BTS(4, 0) {}
     } else if constexpr (BMAX == 20) {
       HPAC_BTS(20, 18) HPAC_BTS(18, 16) HPAC_BTS(16, 14) HPAC_BTS(14, 12) HPAC_BTS(12, 10)
