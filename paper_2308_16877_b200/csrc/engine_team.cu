@@ -570,7 +570,7 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
 #endif
 constexpr int kSegPhase = HPAC_SEG_PHASE;  // levels per phase (= binomial_put_bt)
 #ifndef HPAC_SEG_MARGIN
-#define HPAC_SEG_MARGIN 5  // 2 falls off a cliff (check failures -> whole-warp path), 3 is the fastest
+#define HPAC_SEG_MARGIN 4  // 2 falls off a cliff (check failures -> whole-warp path); 3-4 fastest
 #endif
 constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured boundary
 
@@ -579,6 +579,9 @@ constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured bo
 // stay in steps of 4, HPAC_SEG_COARSE, for the instruction cache)
 #ifndef HPAC_SEG_C
 #define HPAC_SEG_C 0  // 0: by segment width
+#endif
+#ifndef HPAC_SEG_BO12
+#define HPAC_SEG_BO12 1  // upper blocks of 12 nodes as well as 8 and 16
 #endif
 #ifndef HPAC_SEG_COARSE
 #define HPAC_SEG_COARSE 1  // one-band block sizes in steps of 4 also for 2-node chunks
@@ -934,7 +937,7 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
         const int bo = __reduce_max_sync(0xffffffffu, no);
         if (bo > 0 && bo <= 16) {
           Bi2 = bi;
-          Bo2 = bo <= 8 ? 8 : 16;
+          Bo2 = bo <= 8 ? 8 : (HPAC_SEG_BO12 && bo <= 12 ? 12 : 16);
         }
       }
     }
@@ -944,7 +947,10 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     bts_phase2<bi, bo, RN, sizeof(xa) / sizeof(double), SEG, C>(v, xa, L, lo, q, sub, w, check,  \
                                                                ok, cnt, js, top, eps_k);        \
   } else
-      if constexpr (C == 2) {
+      if constexpr (C == 2 && HPAC_SEG_BO12) {
+        HPAC_BTS2(4, 8) HPAC_BTS2(4, 12) HPAC_BTS2(4, 16) HPAC_BTS2(6, 8) HPAC_BTS2(6, 12)
+        HPAC_BTS2(6, 16) HPAC_BTS2(8, 8) HPAC_BTS2(8, 12) HPAC_BTS2(8, 16) {}
+      } else if constexpr (C == 2) {
         HPAC_BTS2(4, 8) HPAC_BTS2(4, 16) HPAC_BTS2(6, 8) HPAC_BTS2(6, 16) HPAC_BTS2(8, 8)
         HPAC_BTS2(8, 16) {}
       } else {
