@@ -566,7 +566,7 @@ __device__ bool binomial_put_bt(double spot, double strike, int N, const LatPara
 // fails, or whose price is too small for the tail cut return false and are
 // priced by the whole-warp path (also a pure function of the option).
 #ifndef HPAC_SEG_PHASE
-#define HPAC_SEG_PHASE 32
+#define HPAC_SEG_PHASE 24  // 16/20/28/32/36/40: 75.7/79.0/88.2/86.6/81.9/82.1 vs 89.2 M options/s
 #endif
 constexpr int kSegPhase = HPAC_SEG_PHASE;  // levels per phase (= binomial_put_bt)
 #ifndef HPAC_SEG_MARGIN
