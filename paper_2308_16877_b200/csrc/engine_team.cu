@@ -583,6 +583,9 @@ constexpr int kSegMargin = HPAC_SEG_MARGIN;  // nodes kept below the measured bo
 #ifndef HPAC_SEG_BO12
 #define HPAC_SEG_BO12 1  // upper blocks of 12 nodes as well as 8 and 16
 #endif
+#ifndef HPAC_SEG_COMBOS
+#define HPAC_SEG_COMBOS 2  // two-band shapes: 0 all nine, 1 without BI 4, 2 without BO 8, 3 neither
+#endif
 #ifndef HPAC_SEG_COARSE
 #define HPAC_SEG_COARSE 1  // one-band block sizes in steps of 4 also for 2-node chunks
 #endif
@@ -929,6 +932,7 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
         ni = lks_ok ? max(1, (jo - lo + SEG - 1) / SEG) : 1 << 20;
         ni = (ni + C - 1) & ~(C - 1);  // whole chunks
         ni = ni < 4 ? 4 : ni;
+        if ((HPAC_SEG_COMBOS == 1 || HPAC_SEG_COMBOS == 3) && ni < 6) ni = 6;
       }
       const int bi = __reduce_max_sync(0xffffffffu, ni);
       if (bi <= 8) {
@@ -937,7 +941,7 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
         const int bo = __reduce_max_sync(0xffffffffu, no);
         if (bo > 0 && bo <= 16) {
           Bi2 = bi;
-          Bo2 = bo <= 8 ? 8 : (HPAC_SEG_BO12 && bo <= 12 ? 12 : 16);
+          Bo2 = bo <= 8 && HPAC_SEG_COMBOS < 2 ? 8 : (HPAC_SEG_BO12 && bo <= 12 ? 12 : 16);
         }
       }
     }
@@ -947,7 +951,15 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     bts_phase2<bi, bo, RN, sizeof(xa) / sizeof(double), SEG, C>(v, xa, L, lo, q, sub, w, check,  \
                                                                ok, cnt, js, top, eps_k);        \
   } else
-      if constexpr (C == 2 && HPAC_SEG_BO12) {
+      if constexpr (C == 2 && HPAC_SEG_BO12 && HPAC_SEG_COMBOS == 3) {
+        HPAC_BTS2(6, 12) HPAC_BTS2(6, 16) HPAC_BTS2(8, 12) HPAC_BTS2(8, 16) {}
+      } else if constexpr (C == 2 && HPAC_SEG_BO12 && HPAC_SEG_COMBOS == 1) {
+        HPAC_BTS2(6, 8) HPAC_BTS2(6, 12) HPAC_BTS2(6, 16) HPAC_BTS2(8, 8) HPAC_BTS2(8, 12)
+        HPAC_BTS2(8, 16) {}
+      } else if constexpr (C == 2 && HPAC_SEG_BO12 && HPAC_SEG_COMBOS == 2) {
+        HPAC_BTS2(4, 12) HPAC_BTS2(4, 16) HPAC_BTS2(6, 12) HPAC_BTS2(6, 16) HPAC_BTS2(8, 12)
+        HPAC_BTS2(8, 16) {}
+      } else if constexpr (C == 2 && HPAC_SEG_BO12) {
         HPAC_BTS2(4, 8) HPAC_BTS2(4, 12) HPAC_BTS2(4, 16) HPAC_BTS2(6, 8) HPAC_BTS2(6, 12)
         HPAC_BTS2(6, 16) HPAC_BTS2(8, 8) HPAC_BTS2(8, 12) HPAC_BTS2(8, 16) {}
       } else if constexpr (C == 2) {
