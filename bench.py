@@ -855,7 +855,7 @@ def our_arm(args, wl, emit=True):
     roof["traffic"] = load_traffic(wl["name"])
     # the same launch against the HBM roofline (north star: every number also
     # as a fraction of HBM); algorithmic bytes per metric item
-    bytes_item = {"binomial": 48.0, "blackscholes": 48.0, "lavamd": 72.0, "kmeans": 260.0}[wl["benchmark"]]
+    bytes_item = {"binomial": 48.0, "blackscholes": 48.0, "lavamd": 104.0, "kmeans": 260.0}[wl["benchmark"]]
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     if wl["benchmark"] == "blackscholes":
         hbm_ach = roof["achieved"]

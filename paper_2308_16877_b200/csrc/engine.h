@@ -64,6 +64,7 @@ struct EngineParams {
   // Blackscholes iACT engine (engine_bs_iact.cu): lookups decide a chunk of
   // q_steps steps, then the CTA prices the queued misses densely
   int32_t q_steps;
+  int32_t box_tile;       // LavaMD: tiled box order (T, 0 = natural order; full grid only)
   double iact_thr2;       // largest ssq with sqrt_rn(ssq) <= iact_thr (exact test, no sqrt)
   // outputs
   uint8_t* paths;

@@ -51,6 +51,17 @@ static inline bool taf_window_in_registers(const EngineParams& p) {
   return p.taf_h <= 8 && engine_thread_max_out(p.region.app) == 1;
 }
 
+// i-th box of the tiled order: tile columns of T x T boxes (x fastest, then
+// y), z-plane by z-plane inside a column; b1 % T == 0
+__device__ __forceinline__ int lava_tile_order(int i, int b1, int T) {
+  const int col = T * T * b1;
+  const int tile = i / col, r = i - tile * col;
+  const int z = r / (T * T), rr = r - z * T * T;
+  const int nt = b1 / T;
+  const int x = (tile % nt) * T + rr % T, y = (tile / nt) * T + rr / T;
+  return x + b1 * (y + b1 * z);
+}
+
 template <class App, int TECH, int HREG, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) engine_thread_kernel(const EngineParams p) {
   extern __shared__ __align__(16) double smem[];
@@ -58,7 +69,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) e
   constexpr int OUT_MAX = App::OUT_MAX;
 
   const int local = threadIdx.x;
-  const int team = p.team_begin + (int)blockIdx.x;
+  // LavaMD: boxes in T x T x all-z tile columns (z-planes of a tile in
+  // order) so a box's 27-neighbourhood is still in L2 from the previous plane;
+  // teams are independent, so the processing order changes nothing else
+  const int team = p.box_tile > 0 ? lava_tile_order((int)blockIdx.x, p.region.lavamd_boxes1d, p.box_tile)
+                                  : p.team_begin + (int)blockIdx.x;
   const int64_t tid = (int64_t)team * p.tpt + local;
   const int64_t owner = p.per_team ? (int64_t)team : tid;  // machine.hpp:77-80
   const int ws = p.ws;

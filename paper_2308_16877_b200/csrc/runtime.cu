@@ -435,6 +435,14 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
     if (g->threads_per_team > 1024)
       return fail(err, el, HPAC_ERR_UNSUPPORTED, "threads_per_team > 1024 is not supported");
     p.per_team = 1;
+    {
+      // tiled box order for L2 reuse of the 27-neighbourhoods (whole grid only;
+      // HPAC_LAVA_TILE=0 keeps the natural order)
+      const char* lt = getenv("HPAC_LAVA_TILE");
+      const int b1 = r.lavamd_boxes1d;
+      const bool whole = tb == 0 && te == g->num_teams && (long long)g->num_teams == boxes && n == boxes;
+      p.box_tile = (lt && strcmp(lt, "0") == 0) || !whole ? 0 : (b1 % 32 == 0 ? 32 : (b1 % 16 == 0 ? 16 : 0));
+    }
     pr.kind = 0;
     pr.block = p.tpt;
     pr.nblocks = te - tb;

@@ -100,3 +100,29 @@ def test_cuda_lavamd_bit_exact_vs_oracle(spec_fn):
         assert lr.stats[f] == getattr(st, f), f
     assert np.array_equal(fv.cpu().numpy(), ofv)
     assert np.array_equal(paths.cpu().numpy(), op)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("b1", [16, 32])
+def test_cuda_lavamd_tiled_box_order_equals_natural(b1, monkeypatch):
+    """Whole-grid launches process boxes in 16/32-wide tile columns (L2 reuse
+    of the neighbourhoods, csrc/engine_thread.cu lava_tile_order); teams are
+    independent, so forces, stats and paths equal the natural order's."""
+    import torch
+    P = 128
+    nb = b1 ** 3
+    rv, qv = E.make_lavamd(b1, P, 11)
+    d_rv, d_qv = torch.from_numpy(rv).cuda(), torch.from_numpy(qv).cuda()
+    grid = E.GridConfig(nb, P, 32, 1)
+    res = []
+    for tile in ["1", "0"]:
+        monkeypatch.setenv("HPAC_LAVA_TILE", tile)
+        fv = torch.zeros((nb * P, 4), dtype=torch.float64, device="cuda")
+        paths = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        lr = E.run_region(grid, nb, 1, E.lavamd_region(d_rv, d_qv, fv, b1, P),
+                          E.taf(3, 8, 0.1, "warp"), paths=paths)
+        res.append((lr.stats, fv.cpu().numpy(), paths.cpu().numpy()))
+    for f in STAT_FIELDS:
+        assert res[0][0][f] == res[1][0][f], f
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][2], res[1][2])
