@@ -1470,6 +1470,130 @@ __global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS) binomial_
 //  3. binomial_resolve_kernel: every hit copies its producer's price.
 // Exact (spec NULL) launches price every item of the team range directly.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Binomial TAF for American puts: 8 teams per CTA, one per 8-lane segment.
+// TAF decisions depend on the prices (taf.hpp:59-163), so each team's item
+// stream is sequential; the teams are independent, so a warp runs four of
+// them side by side: every step each segment either emits its team's last
+// price (TafState::emit_approx) or prices its team's option in the shared
+// binomial_put_seg call (idle segments skip the lattice), then runs the TAF
+// state machine on its own shared-memory window ring. Prices are the exact
+// path's (same function of the option), so decisions replay bit-exactly.
+// ---------------------------------------------------------------------------
+constexpr int kTafTeamsPerWarp = 32 / kBinoSegW;
+
+__global__ void __launch_bounds__(kBinoWarps * 32, HPAC_BINO_MIN_CTAS)
+    binomial_taf_seg_kernel(const EngineParams p, int team_end) {
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / kBinoSegW, sub = lane % kBinoSegW;
+  const int N = p.region.binomial_steps;
+  const int team = p.team_begin + ((int)blockIdx.x * kBinoWarps + warp) * kTafTeamsPerWarp + g;
+  const bool mine = team < team_end;
+  const int h = p.taf_h;
+  double* xch = smem + warp * 32 * kLatBmax;  // 4 segment windows / whole-warp fallback
+  double* ring = smem + kBinoWarps * 32 * kLatBmax + (warp * kTafTeamsPerWarp + g) * h;
+  const int64_t G = p.stride;
+  const int64_t trip = mine ? trip_count(team, G, p.n, p.steps) : 0;
+  const unsigned long long tpt = (unsigned long long)p.tpt, wpt = (unsigned long long)p.wpt;
+  int mode = kTafFilling, rem = 0, cnt = 0, head = 0;
+  double lastv = 0.0;
+  unsigned long long tot = 0, app = 0, ws = 0;
+  bool err = false;
+  // the warp walks the longest of its teams' streams
+  int64_t tmax = trip;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t ot = __shfl_xor_sync(0xffffffffu, tmax, o);
+    tmax = ot > tmax ? ot : tmax;
+  }
+  for (int64_t step = 0; step < tmax; ++step) {
+    const bool active = step < trip;
+    const int64_t idx = team + step * G;
+    const bool approx = active && mode == kTafPredicting;
+    const bool want = active && !approx;
+    double o[5] = {100.0, 100.0, 0.05, 0.25, 1.0};
+    if (want) {
+#pragma unroll
+      for (int d = 0; d < 5; ++d) o[d] = __ldg(p.region.in + idx * 5 + d);
+    }
+    double v = 0.0;
+    unsigned long long nodes = 0;
+    const bool okseg = binomial_put_seg<kBinoSegW, SegWin<kBinoSegW>::BMAX>(
+        o, want, N, xch + g * SegWin<kBinoSegW>::WIN, v, nodes);
+    if (want && okseg && sub == 0) atomicAdd(&p.counters[kCntLatticeNodes], nodes);
+    // options the segment path declines: the whole-warp path, one at a time
+    unsigned fb = __ballot_sync(0xffffffffu, want && !okseg && sub == 0);
+    while (fb) {
+      const int gg = (__ffs(fb) - 1) / kBinoSegW;
+      fb &= fb - 1;
+      const double oo[5] = {__shfl_sync(0xffffffffu, o[0], gg * kBinoSegW),
+                            __shfl_sync(0xffffffffu, o[1], gg * kBinoSegW),
+                            __shfl_sync(0xffffffffu, o[2], gg * kBinoSegW),
+                            __shfl_sync(0xffffffffu, o[3], gg * kBinoSegW),
+                            __shfl_sync(0xffffffffu, o[4], gg * kBinoSegW)};
+      bool ok;
+      const double vv = binomial_warp_price<kLatBmax, true, true>(oo, N, xch, ok,
+                                                                  &p.counters[kCntLatticeFallback]);
+      if (g == gg) {
+        v = vv;
+        if (!ok) err = true;
+      }
+    }
+    double outv = 0.0;
+    if (approx) {
+      // TafState::emit_approx, taf.hpp:114-117
+      outv = lastv;
+      if (--rem == 0) {
+        cnt = 0;
+        head = 0;
+        mode = kTafFilling;
+      }
+    } else if (want) {
+      // TafState::observe_accurate, taf.hpp:94-108 (ring in shared memory)
+      outv = v;
+      if (sub == 0) {
+        int slot;
+        if (cnt < h) {
+          slot = head + cnt;
+          if (slot >= h) slot -= h;
+        } else {
+          slot = head;
+        }
+        ring[slot] = v;
+      }
+      if (cnt < h) ++cnt; else head = head + 1 == h ? 0 : head + 1;
+      lastv = v;
+    }
+    __syncwarp();
+    if (want) {
+      if (mode == kTafPredicting) {
+        if (--rem == 0) {
+          cnt = 0;
+          head = 0;
+          mode = kTafFilling;
+        }
+      } else if ((mode == kTafFilling && cnt == h) || mode == kTafChecking) {
+        if (taf_ring_passes(ring, 1, h, head, cnt, p.taf_thr)) {
+          rem = p.taf_p;
+          mode = kTafPredicting;
+        } else {
+          mode = kTafChecking;
+        }
+      }
+    }
+    if (active && sub == 0) {
+      if (p.region.out) p.region.out[idx] = outv;
+      if (p.paths) p.paths[idx] = approx ? 1 : 0;
+      tot += tpt;
+      ws += wpt;
+      if (approx) app += tpt;
+    }
+    __syncwarp();
+  }
+  flush_stats(p, tot, app, ws, (sub == 0 && trip > 0) ? wpt : 0ull, err);
+}
+
 struct BinoWork {
   int* act;        // [n] producing step of a hit (>= 0), -1 priced, -2 skipped (iACT only)
   int* miss;       // [n] items to price (iACT / perforation)
@@ -1832,6 +1956,22 @@ static cudaError_t launch_bino2(const EngineParams& p, int nblocks, size_t smem,
   // the prices); HPAC_BINO_PIPELINE=0 keeps the one-kernel chunked engine
   const char* pe = getenv("HPAC_BINO_PIPELINE");
   const int ts = p.tsize > 0 ? p.tsize : 1;
+  if (TECH == HPAC_TECH_TAF && am && put && kBinoSeg > 0 &&
+      p.region.binomial_steps + 1 <= 32 * kLatBmax && !(pe && strcmp(pe, "0") == 0)) {
+    // 8 teams per CTA, one per 8-lane segment (binomial_taf_seg_kernel)
+    const size_t tsm = ((size_t)kBinoWarps * 32 * kLatBmax +
+                        (size_t)kBinoWarps * kTafTeamsPerWarp * (p.taf_h > 0 ? p.taf_h : 1)) *
+                       sizeof(double);
+    if (tsm > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(binomial_taf_seg_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      if (e != cudaSuccess) return e;
+    }
+    const int per = kBinoWarps * kTafTeamsPerWarp;
+    binomial_taf_seg_kernel<<<(nblocks + per - 1) / per, kBinoWarps * 32, tsm, st>>>(
+        p, p.team_begin + nblocks);
+    return cudaGetLastError();
+  }
   if (TECH != HPAC_TECH_TAF && !(pe && strcmp(pe, "0") == 0) && p.n < (1ll << 31) &&
       4 * (size_t)bino_decide_warp_doubles(ts) * sizeof(double) <= 200 * 1024) {
     if (am && put) return launch_bino_pipeline<true, true>(p, nblocks, st);

@@ -1,6 +1,6 @@
 """The binomial decide -> price -> resolve launch (csrc/engine_team.cu,
-launch_bino_pipeline) against the one-kernel chunked engine
-(HPAC_BINO_PIPELINE=0) and the oracle: identical stats, path bits and prices
+launch_bino_pipeline) and the 8-teams-per-CTA TAF kernel against the
+one-kernel chunked engine (HPAC_BINO_PIPELINE=0) and the oracle: identical stats, path bits and prices
 for exact, iACT and perforation runs, American/European puts and calls,
 lattices below and above the register bound, ragged grids and team ranges.
 Both engines price an option with the same function of the option alone
@@ -36,7 +36,10 @@ CASES = [  # (teams, ipt, n, lattice steps)
 ]
 SPECS = [lambda: None, lambda: E.iact(4, 0.4, level="team"), lambda: E.iact(1, 0.0, level="team"),
          lambda: E.iact(8, float("inf"), level="team"), lambda: E.perfo("small", 3),
-         lambda: E.perfo("random", 40, seed=3)]
+         lambda: E.perfo("random", 40, seed=3),
+         # TAF: 8 teams per CTA (binomial_taf_seg_kernel) vs one team per CTA
+         lambda: E.taf(2, 4, 0.01, "team"), lambda: E.taf(3, 2, float("inf"), "team"),
+         lambda: E.taf(5, 1, 0.5, "team")]
 
 
 @pytest.mark.parametrize("case", CASES)
