@@ -36,6 +36,9 @@
 // encounters / barrier flags.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "apps.cuh"
 #include "engine.h"
 #include "hpac_device.cuh"
@@ -369,6 +372,227 @@ __global__ void __launch_bounds__(kIactMaxT) bs_iact_kernel(const EngineParams p
   }
 }
 
+// ---------------------------------------------------------------------------
+// Per-lane tables (tables_per_warp == warp_size, the default), thread or warp
+// level: no lane ever reads another lane's table, so the table lives in the
+// lane's registers and the whole decision stream of a chunk of 32 steps runs
+// without shared memory or barriers (warp votes are one ballot per step). The
+// warp then prices its chunk's misses densely (two per thread) into a shared
+// 32 x 32 output tile, resolves the hits (a producer earlier in the chunk
+// from the tile, an older one from the slot's remembered price), and stores
+// the tile coalesced. Warps are independent: one CTA = one team.
+// ---------------------------------------------------------------------------
+constexpr int kLaneChunk = 32;
+
+template <int LEVEL, int TS>
+__global__ void __launch_bounds__(kIactMaxT) bs_iact_lane_kernel(const EngineParams p) {
+  extern __shared__ __align__(16) double smem[];
+  const int local = threadIdx.x;
+  const int warp = local >> 5, lane = local & 31;
+  const int team = p.team_begin + (int)blockIdx.x;
+  const int64_t tid = (int64_t)team * p.tpt + local;
+  const int64_t G = p.stride;
+  const int ws = p.ws;
+  const int sl = lane % ws;  // logical lane
+  const unsigned seg_mask = ws >= 32 ? 0xffffffffu : (((1u << ws) - 1u) << (lane - sl));
+  const double thr2 = p.iact_thr2;
+  const double* __restrict__ in = p.region.in;
+  double* __restrict__ out = p.region.out;
+  // per-warp shared tile: outputs [32 steps][32 lanes], hit producers, miss list
+  double* tile = smem + warp * (kLaneChunk * 32 + kLaneChunk * 32 / 8 + kLaneChunk * 32 / 4);
+  signed char* hsrc = reinterpret_cast<signed char*>(tile + kLaneChunk * 32);          // [s][lane]
+  short* mlist = reinterpret_cast<short*>(tile + kLaneChunk * 32 + kLaneChunk * 32 / 8);  // [<=1024]
+
+  double tab[TS][kRecD];
+  int sstep[TS];   // producing step of each slot
+  double sval[TS]; // its price, once known (chunks before the current one)
+#pragma unroll
+  for (int k = 0; k < TS; ++k) {
+    sstep[k] = -1;
+    sval[k] = 0.0;
+#pragma unroll
+    for (int c = 0; c < kRecD; ++c) tab[k][c] = 0.0;
+  }
+  int rr = 0, occ = 0;
+  unsigned c_total = 0, c_approx = 0, c_warp = 0, c_div = 0;
+  bool touched = false, app_error = false;
+  const int nsteps = (int)p.steps;
+
+  for (int c0 = 0; c0 < nsteps; c0 += kLaneChunk) {
+    const int cs = nsteps - c0 < kLaneChunk ? nsteps - c0 : kLaneChunk;
+    unsigned act_m = 0, apx_m = 0, miss_m = 0;
+    // ---- decisions: lookup (iact.hpp:58-110), vote, table insert
+    double xn[kRecD];
+    {
+      const int64_t idx0 = tid + (int64_t)c0 * G;
+      if (idx0 < p.n) {
+#pragma unroll
+        for (int c = 0; c < kRecD; ++c) xn[c] = __ldg(in + idx0 * kRecD + c);
+      }
+    }
+    for (int s = 0; s < cs; ++s) {
+      const int step = c0 + s;
+      const int64_t idx = tid + (int64_t)step * G;
+      const bool active = idx < p.n;
+      double x[kRecD];
+#pragma unroll
+      for (int c = 0; c < kRecD; ++c) x[c] = xn[c];
+      if (s + 1 < cs && idx + G < p.n) {  // next step's record in flight during this lookup
+#pragma unroll
+        for (int c = 0; c < kRecD; ++c) xn[c] = __ldg(in + (idx + G) * kRecD + c);
+      }
+      int near = -1;
+      double near_q = dinf();
+      double q[TS];
+#pragma unroll
+      for (int k = 0; k < TS; ++k) {
+        double ssq = 0.0;
+#pragma unroll
+        for (int c = 0; c < kRecD; ++c) {
+          const double df = __dsub_rn(tab[k][c], x[c]);
+          ssq = __dadd_rn(ssq, __dmul_rn(df, df));
+        }
+        q[k] = ssq;
+      }
+#pragma unroll
+      for (int k = 0; k < TS; ++k) {
+        if (active && k < occ && q[k] < near_q) {
+          bool take = true;
+          if (near >= 0 && q[k] >= near_q * (1.0 - 0x1p-48))
+            take = __dsqrt_rn(q[k]) < __dsqrt_rn(near_q);
+          if (take) {
+            near_q = q[k];
+            near = k;
+          }
+        }
+      }
+      const bool pred = active && near >= 0 && near_q <= thr2;
+      bool approx = pred;
+      if (LEVEL == HPAC_LEVEL_WARP) {
+        const unsigned bv = __ballot_sync(0xffffffffu, pred) & seg_mask;
+        const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
+        approx = 2 * __popc(bv) > __popc(ba);
+      }
+      signed char hs = -1;
+      if (active) {
+        if (approx && near < 0) approx = false;  // empty table: accurate fallback
+        if (approx) {
+          // the slot's output (nearest slot when forced): a producer in this
+          // chunk is resolved after pricing, an older one's price is known
+          int ps = 0;
+          double pv = 0.0;
+#pragma unroll
+          for (int k = 0; k < TS; ++k)
+            if (k == near) {
+              ps = sstep[k];
+              pv = sval[k];
+            }
+          if (ps >= c0) hs = (signed char)(ps - c0);
+          else tile[s * 32 + lane] = pv;
+        } else {
+          miss_m |= 1u << s;
+          if (!pred) {  // writer (one lane per table): insert at the cursor
+#pragma unroll
+            for (int k = 0; k < TS; ++k)
+              if (k == rr) {
+#pragma unroll
+                for (int c = 0; c < kRecD; ++c) tab[k][c] = x[c];
+                sstep[k] = step;
+              }
+            rr = rr + 1 == TS ? 0 : rr + 1;
+            occ = occ + 1 < TS ? occ + 1 : TS;
+          }
+        }
+        act_m |= 1u << s;
+        if (approx) apx_m |= 1u << s;
+        if (p.paths) p.paths[idx] = approx ? 1 : 0;
+      }
+      hsrc[s * 32 + lane] = hs;
+    }
+    // ---- warp stats (cost.hpp:66-86)
+    for (int s = 0; s < cs; ++s) {
+      const unsigned ba = __ballot_sync(0xffffffffu, (act_m >> s) & 1u) & seg_mask;
+      const unsigned bx = __ballot_sync(0xffffffffu, (apx_m >> s) & 1u) & seg_mask;
+      if (sl == 0 && ba) {
+        touched = true;
+        c_warp += 1;
+        if (bx != 0 && bx != ba) c_div += 1;
+      }
+    }
+    c_total += __popc(act_m);
+    c_approx += __popc(apx_m);
+    // ---- the warp's misses, densely: exclusive scan of the per-lane counts
+    const int mine = __popc(miss_m);
+    int off = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, off, o);
+      if (lane >= o) off += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= mine;
+    for (unsigned m = miss_m; m; m &= m - 1) mlist[off++] = (short)((__ffs(m) - 1) * 32 + lane);
+    __syncwarp();
+    for (int i = lane; i < total; i += 64) {
+      const int j = i + 32 < total ? i + 32 : i;
+      const int e0 = mlist[i], e1 = mlist[j];
+      const int64_t t0 = tid - lane + (e0 & 31) + (int64_t)(c0 + (e0 >> 5)) * G;
+      const int64_t t1 = tid - lane + (e1 & 31) + (int64_t)(c0 + (e1 >> 5)) * G;
+      double a[kRecD], b[kRecD];
+#pragma unroll
+      for (int c = 0; c < kRecD; ++c) {
+        a[c] = __ldg(in + t0 * kRecD + c);
+        b[c] = __ldg(in + t1 * kRecD + c);
+      }
+      double v0, v1;
+      const bool ok0 = bs_call(a[0], a[1], a[2], a[3], a[4], v0);
+      const bool ok1 = bs_call(b[0], b[1], b[2], b[3], b[4], v1);
+      if (!ok0 || !ok1) app_error = true;
+      tile[(e0 >> 5) * 32 + (e0 & 31)] = v0;
+      if (j != i) tile[(e1 >> 5) * 32 + (e1 & 31)] = v1;
+    }
+    __syncwarp();
+    // ---- hits from producers in this chunk, remembered slot prices, store
+    for (int s = 0; s < cs; ++s) {
+      const int h = hsrc[s * 32 + lane];
+      if (h >= 0) tile[s * 32 + lane] = tile[h * 32 + lane];
+    }
+#pragma unroll
+    for (int k = 0; k < TS; ++k)
+      if (sstep[k] >= c0) sval[k] = tile[(sstep[k] - c0) * 32 + lane];
+    if (out)
+      for (int s = 0; s < cs; ++s)
+        if ((act_m >> s) & 1u) __stcs(out + tid + (int64_t)(c0 + s) * G, tile[s * 32 + lane]);
+    __syncwarp();
+  }
+
+  const unsigned long long s_total = warp_sum(c_total);
+  const unsigned long long s_approx = warp_sum(c_approx);
+  const unsigned long long s_warp = warp_sum(c_warp);
+  const unsigned long long s_div = warp_sum(c_div);
+  const unsigned long long s_res = warp_sum((sl == 0 && touched) ? 1u : 0u);
+  const unsigned any_err = __ballot_sync(0xffffffffu, app_error);
+  if (lane == 0) {
+    if (s_total) atomicAdd(&p.counters[kCntTotal], s_total);
+    if (s_approx) atomicAdd(&p.counters[kCntApprox], s_approx);
+    if (s_div) atomicAdd(&p.counters[kCntDivergent], s_div);
+    if (s_warp) atomicAdd(&p.counters[kCntWarpSteps], s_warp);
+    if (s_res) atomicAdd(&p.counters[kCntResidentWarps], s_res);
+    if (any_err) atomicAdd(&p.counters[kCntAppError], 1ull);
+  }
+}
+
+static bool bs_iact_lane_eligible(const EngineParams& p) {
+  const char* e = getenv("HPAC_IACT_LANE");
+  return !(e && strcmp(e, "0") == 0) && p.tpw == p.ws && p.level != HPAC_LEVEL_TEAM &&
+         (p.tsize == 1 || p.tsize == 2 || p.tsize == 4 || p.tsize == 8);
+}
+
+static size_t bs_iact_lane_smem(const EngineParams& p) {
+  return (size_t)(p.tpt / 32) * (kLaneChunk * 32 + kLaneChunk * 32 / 8 + kLaneChunk * 32 / 4) *
+         sizeof(double);
+}
+
 bool engine_bs_iact_eligible(const EngineParams& p) {
   return p.region.app == HPAC_APP_BLACKSCHOLES && p.tech == HPAC_TECH_IACT && !p.per_team &&
          !p.has_enc && !p.barrier_eval && p.fast_ws && p.tpt % 32 == 0 && p.tpt <= kIactMaxT &&
@@ -376,6 +600,7 @@ bool engine_bs_iact_eligible(const EngineParams& p) {
 }
 
 size_t engine_bs_iact_smem(EngineParams& p) {
+  if (bs_iact_lane_eligible(p)) return bs_iact_lane_smem(p);
   p.q_steps = kQueueItems / p.tpt > 0 ? kQueueItems / p.tpt : 1;
   const IactLayout L = iact_layout(p.tpt, p.wpt * p.tpw, p.tsize, p.q_steps);
   return (size_t)L.total * sizeof(double);
@@ -388,8 +613,26 @@ static auto bs_iact_pick(const EngineParams& p) {
                   : bs_iact_kernel<HPAC_LEVEL_THREAD, TS>;
 }
 
+template <int TS>
+static auto bs_iact_lane_pick(const EngineParams& p) {
+  return p.level == HPAC_LEVEL_WARP && p.voting ? bs_iact_lane_kernel<HPAC_LEVEL_WARP, TS>
+                                                : bs_iact_lane_kernel<HPAC_LEVEL_THREAD, TS>;
+}
+
 cudaError_t engine_bs_iact_launch(const EngineParams& p, int nblocks, size_t smem,
                                   cudaStream_t st) {
+  if (bs_iact_lane_eligible(p)) {
+    auto k = p.tsize == 1   ? bs_iact_lane_pick<1>(p)
+             : p.tsize == 2 ? bs_iact_lane_pick<2>(p)
+             : p.tsize == 4 ? bs_iact_lane_pick<4>(p)
+                            : bs_iact_lane_pick<8>(p);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k<<<nblocks, p.tpt, smem, st>>>(p);
+    return cudaGetLastError();
+  }
   // table slots unrolled for the common sizes; the table's smem contents are
   // only read below occ, so unrolled reads past occ see stale but unused data
   auto k = p.tsize == 1   ? bs_iact_pick<1>(p)

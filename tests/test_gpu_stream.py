@@ -160,3 +160,33 @@ def test_paired_stream_kernel_equals_unpaired(shape, si, monkeypatch):
         assert a[0].stats[f] == b[0].stats[f], f
     assert np.array_equal(a[1], b[1])
     assert np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[1], SHAPES[3], SHAPES[4]])
+@pytest.mark.parametrize("spec_fn", [lambda: E.iact(1, 0.5), lambda: E.iact(2, 0.5),
+                                     lambda: E.iact(4, 0.3, None, "warp"), lambda: E.iact(8, 0.2),
+                                     lambda: E.iact(2, float("inf"), None, "warp"),
+                                     lambda: E.iact(4, 0.0)])
+def test_iact_lane_tables_equal_shared_tables(shape, spec_fn, monkeypatch):
+    # per-lane tables in registers (bs_iact_lane_kernel) vs shared-memory
+    # tables (bs_iact_kernel, HPAC_IACT_LANE=0) vs the lockstep engine
+    teams, tpt, ws, ipt, n = shape
+    opts = E.make_bs_portfolio(n, 17)
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    try:
+        a = _run(grid, n, d_opts, spec_fn)
+    except E.ArenaOverflowError:
+        # the reference's arena charge applies whatever the engine
+        monkeypatch.setenv("HPAC_IACT_LANE", "0")
+        with pytest.raises(E.ArenaOverflowError):
+            _run(grid, n, d_opts, spec_fn)
+        return
+    monkeypatch.setenv("HPAC_IACT_LANE", "0")
+    b = _run(grid, n, d_opts, spec_fn)
+    c = _run(grid, n, d_opts, spec_fn, engine="thread")
+    for r in (b, c):
+        for f in STAT_FIELDS:
+            assert a[0].stats[f] == r[0].stats[f], f
+        assert np.array_equal(a[1], r[1])
+        assert np.array_equal(a[2], r[2])
