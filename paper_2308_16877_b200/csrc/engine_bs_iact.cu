@@ -384,8 +384,14 @@ __global__ void __launch_bounds__(kIactMaxT) bs_iact_kernel(const EngineParams p
 // ---------------------------------------------------------------------------
 constexpr int kLaneChunk = 32;
 
+#ifndef HPAC_IACT_LANE_MINB
+#define HPAC_IACT_LANE_MINB 1  // min 256-thread-equivalent blocks (register cap)
+#endif
+#ifndef HPAC_IACT_LANE_PAIR
+#define HPAC_IACT_LANE_PAIR 1  // price two misses per iteration
+#endif
 template <int LEVEL, int TS>
-__global__ void __launch_bounds__(kIactMaxT) bs_iact_lane_kernel(const EngineParams p) {
+__global__ void __launch_bounds__(kIactMaxT, HPAC_IACT_LANE_MINB) bs_iact_lane_kernel(const EngineParams p) {
   extern __shared__ __align__(16) double smem[];
   const int local = threadIdx.x;
   const int warp = local >> 5, lane = local & 31;
@@ -533,8 +539,8 @@ __global__ void __launch_bounds__(kIactMaxT) bs_iact_lane_kernel(const EnginePar
     off -= mine;
     for (unsigned m = miss_m; m; m &= m - 1) mlist[off++] = (short)((__ffs(m) - 1) * 32 + lane);
     __syncwarp();
-    for (int i = lane; i < total; i += 64) {
-      const int j = i + 32 < total ? i + 32 : i;
+    for (int i = lane; i < total; i += (HPAC_IACT_LANE_PAIR ? 64 : 32)) {
+      const int j = HPAC_IACT_LANE_PAIR && i + 32 < total ? i + 32 : i;
       const int e0 = mlist[i], e1 = mlist[j];
       const int64_t t0 = tid - lane + (e0 & 31) + (int64_t)(c0 + (e0 >> 5)) * G;
       const int64_t t1 = tid - lane + (e1 & 31) + (int64_t)(c0 + (e1 >> 5)) * G;
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(kIactMaxT) bs_iact_lane_kernel(const EnginePar
       }
       double v0, v1;
       const bool ok0 = bs_call(a[0], a[1], a[2], a[3], a[4], v0);
-      const bool ok1 = bs_call(b[0], b[1], b[2], b[3], b[4], v1);
+      const bool ok1 = HPAC_IACT_LANE_PAIR ? bs_call(b[0], b[1], b[2], b[3], b[4], v1) : true;
       if (!ok0 || !ok1) app_error = true;
       tile[(e0 >> 5) * 32 + (e0 & 31)] = v0;
       if (j != i) tile[(e1 >> 5) * 32 + (e1 & 31)] = v1;
