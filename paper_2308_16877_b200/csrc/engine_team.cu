@@ -976,7 +976,11 @@ __device__ bool binomial_put_seg(const double (&o)[5], bool has, int N, double* 
     bts_phase<(b), BMAX, SEG, C, RN, sizeof(xa) / sizeof(double)>(v, xa, L, lo, q, sub, w, check, \
                                                                   ok, cnt, js, top, eps_k);    \
   } else
-    if constexpr (C == 4 || (C == 2 && BMAX == 20 && HPAC_SEG_COARSE)) {
+    if constexpr (C == 2 && BMAX == 20 && HPAC_SEG_COARSE == 2) {
+      HPAC_BTS(20, 12) HPAC_BTS(12, 4) HPAC_BTS(4, 0) {}
+    } else if constexpr (C == 2 && BMAX == 20 && HPAC_SEG_COARSE == 3) {
+      HPAC_BTS(20, 10) HPAC_BTS(10, 0) {}
+    } else if constexpr (C == 4 || (C == 2 && BMAX == 20 && HPAC_SEG_COARSE)) {
       HPAC_BTS(20, 16) HPAC_BTS(16, 12) HPAC_BTS(12, 8) HPAC_BTS(8, 4) HPAC_BTS(4, 0) {}
     } else if constexpr (BMAX == 20) {
       HPAC_BTS(20, 18) HPAC_BTS(18, 16) HPAC_BTS(16, 14) HPAC_BTS(14, 12) HPAC_BTS(12, 10)
