@@ -128,9 +128,8 @@ def kmeans_filter_flops(d, k):
     return 2.0 * d * k + 2.0 * d + 3.0 * k
 
 
-# LavaMD pair term (apps.cuh AppLavaMD::eval): dot 5, r2 2, exponent arg 1,
-# exp 30 (reduction 5, degree-12 Horner 24, scale 1), q*vij 1, 2qv 1, fv 1,
-# d 3, f 6 = 50 FP64 flops per particle pair
+# LavaMD pair term: SURVEY §8(d)'s algorithmic ~40 FP64 flops per particle
+# pair (Rodinia's pair term with its exp); our restatement executes 45.3
 LAVAMD_PAIR_FLOPS = 40.0  # ~40 per pair (Rodinia pair term with exp); executed: 45.3 (profiles/r03_lavamd_flops.txt)
 
 
