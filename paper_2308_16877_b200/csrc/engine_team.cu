@@ -642,6 +642,7 @@ __device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int
   const bool last = sub == SEG - 1;
   double vr = __shfl_down_sync(0xffffffffu, v[0], 1, SEG);
   if (last) vr = 0.0;  // the segment's top node: right neighbour 0
+  unsigned long long okx = 0;  // bit difference of node lo from its exercise value
   for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
     if (done > 0) {
       sinv *= q.rinv;
@@ -672,11 +673,12 @@ __device__ __forceinline__ void bts_phase(double (&v)[RN], double (&xa)[XN], int
     }
     v[0] = v0;
     vr = last ? 0.0 : nv;
-    ok = ok && !(check && v[0] != xa[0]);  // node lo stays exercised (sub 0)
+    okx |= __double_as_longlong(v[0]) ^ __double_as_longlong(xa[0]);  // node lo exercised (sub 0)
     sq *= q.qd;
     L_last = L;
     --L;
   }
+  if (check && okx != 0) ok = false;
   int cnt = 0, js = -1;
 #pragma unroll
   for (int k = 0; k < B / C; ++k) {
@@ -740,6 +742,7 @@ __device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], in
     ri = last ? c : a;
     ro = last ? 0.0 : b;
   }
+  unsigned long long okx = 0;  // bit difference of node lo from its exercise value
   for (int done = 0; L >= 0 && done < kSegPhase; ++done) {
     if (done > 0) {
       sinv *= q.rinv;
@@ -781,11 +784,12 @@ __device__ __forceinline__ void bts_phase2(double (&r)[RN], double (&xa)[XN], in
     vo[0] = vo0;
     ri = last ? nc : na;
     ro = last ? 0.0 : nb;
-    ok = ok && !(check && vi[0] != xa[0]);  // node lo stays exercised (sub 0)
+    okx |= __double_as_longlong(vi[0]) ^ __double_as_longlong(xa[0]);  // node lo exercised (sub 0)
     sq *= q.qd;
     L_last = L;
     --L;
   }
+  if (check && okx != 0) ok = false;
   int cnt = 0, js = -1;
 #pragma unroll
   for (int k = 0; k < BI / C; ++k) {
