@@ -860,8 +860,12 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
     d.in = (const double*)dalloc(in_bytes, r.in, true, "inputs");
     d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true, "table_out");
     d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true, "encounters");
-    // outputs start from the caller's contents (skipped items keep them)
-    d.out = (double*)dalloc(out_bytes, r.out, true, "outputs");
+    // outputs start from the caller's contents where an item can be left
+    // untouched (perforation skips, accumulating stores, LavaMD's fv +=);
+    // the option regions otherwise write every item, so nothing is copied in
+    const bool keeps = (spec && spec->technique == HPAC_TECH_PERFO) ||
+                       !(r.app == HPAC_APP_BLACKSCHOLES || r.app == HPAC_APP_BINOMIAL);
+    d.out = (double*)dalloc(out_bytes, r.out, keeps, "outputs");
     d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true, "centroids");
     d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true, "labels");
   }

@@ -71,3 +71,20 @@ def test_kmeans_labels_zero_copy(spec_fn):
         assert r.stats["zero_copy"] == (0 if staged else 1)
         labs.append(h_lab.clone())
     assert torch.equal(labs[0], labs[1])
+
+
+@pytest.mark.parametrize("spec_fn,keeps", [(lambda: None, False), (lambda: E.iact(4, 0.4, level="team"), False),
+                                           (lambda: E.perfo("small", 3), True)])
+def test_binomial_host_entry_outputs(spec_fn, keeps):
+    # staged host entry: without perforation every item is written, so the
+    # caller's output buffer is not copied in; perforation keeps skipped items
+    n, steps = 24 * 16, 128
+    opts = E.make_binomial_portfolio(n, 8)
+    grid, mp = E.resolve_grid("binomial", n, items_per_thread=16)
+    out = np.full(n, -7.0)
+    r = E.run_region_host(grid, n, mp, E.binomial_region(opts, steps, out), spec_fn())
+    d_out = torch.full((n,), -7.0, dtype=torch.float64, device="cuda")
+    rd = E.run_region(grid, n, mp, E.binomial_region(torch.from_numpy(opts).cuda(), steps, d_out), spec_fn())
+    assert np.array_equal(out, d_out.cpu().numpy())
+    assert r.stats["approx_invocations"] == rd.stats["approx_invocations"]
+    assert bool((out == -7.0).any()) == keeps
