@@ -190,3 +190,23 @@ def test_iact_lane_tables_equal_shared_tables(shape, spec_fn, monkeypatch):
             assert a[0].stats[f] == r[0].stats[f], f
         assert np.array_equal(a[1], r[1])
         assert np.array_equal(a[2], r[2])
+
+
+@pytest.mark.parametrize("spec_fn", [lambda: E.iact(2, 0.5), lambda: E.iact(4, 0.3, None, "warp"),
+                                     lambda: E.iact(8, 0.2), lambda: E.iact(1, 0.5, None, "warp")])
+@pytest.mark.parametrize("shape", [(8, 64, 32, 50, 8 * 64 * 50 - 37), (5, 32, 8, 97, 5 * 32 * 97)])
+def test_iact_lane_tables_across_chunks(shape, spec_fn, monkeypatch):
+    # more than 32 steps per thread: the lane-table kernel decides in chunks of
+    # 32 and carries each slot's price across chunks (hits on older producers)
+    teams, tpt, ws, ipt, n = shape
+    opts = E.make_bs_portfolio(n, 23)
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    a = _run(grid, n, d_opts, spec_fn)
+    b = _run(grid, n, d_opts, spec_fn, engine="thread")
+    for f in STAT_FIELDS:
+        assert a[0].stats[f] == b[0].stats[f], f
+    assert np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2])
+    if teams * tpt == 512:  # G = the portfolio's 512-option base block: hits every step
+        assert a[0].stats["approx_invocations"] > 0
