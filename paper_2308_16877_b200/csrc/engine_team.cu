@@ -1826,40 +1826,45 @@ static cudaError_t launch_bino_pipeline(const EngineParams& p, int nblocks, cuda
   wk.ctr = reinterpret_cast<unsigned*>(ws);
   wk.act = iact ? reinterpret_cast<int*>(ws + 16) : nullptr;
   wk.miss = (iact || perfo) ? reinterpret_cast<int*>(ws + 16 + (iact ? n * sizeof(int) : 0)) : nullptr;
-  if ((e = cudaMemsetAsync(ws, 0, 16, st)) != cudaSuccess) return e;
+  // every error path below releases the workspace
+  auto fail_free = [&](cudaError_t err) {
+    cudaFreeAsync(ws, st);
+    return err;
+  };
+  if ((e = cudaMemsetAsync(ws, 0, 16, st)) != cudaSuccess) return fail_free(e);
   if (iact || perfo) {
     const int ts = p.tsize > 0 ? p.tsize : 1;
     const size_t dsm = 4 * (size_t)bino_decide_warp_doubles(ts) * sizeof(double);
     auto kd = iact ? binomial_decide_kernel<HPAC_TECH_IACT> : binomial_decide_kernel<HPAC_TECH_PERFO>;
     if (dsm > 48 * 1024 &&
         (e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)) != cudaSuccess)
-      return e;
+      return fail_free(e);
     kd<<<(nblocks + 3) / 4, 128, dsm, st>>>(p, team_end, wk);
   } else {
     binomial_exact_stats_kernel<<<(nblocks + 255) / 256 < 148 ? (nblocks + 255) / 256 : 148, 256, 0, st>>>(p, team_end);
   }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_free(e);
   // persistent pricing grid: every resident CTA slot, at most one per batch
   auto kp = binomial_price_kernel<AM, PUT>;
   const size_t psm = (size_t)kBinoWarps * (big ? 2 * (N + 2) : 32 * kLatBmax) * sizeof(double);
   if (psm > 48 * 1024 &&
       (e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)) != cudaSuccess)
-    return e;
+    return fail_free(e);
   int per_sm = 0, dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kBinoWarps * 32, psm)) != cudaSuccess)
-    return e;
+    return fail_free(e);
   const long long items = (long long)nblocks * p.steps;
   const int nseg = (AM && PUT && kBinoSeg > 0 && !big) ? 32 / kBinoSegW : 1;
   long long grid = (long long)(per_sm > 0 ? per_sm : 1) * sms;
   const long long need = (items + (long long)nseg * kBinoWarps - 1) / ((long long)nseg * kBinoWarps);
   if (grid > need) grid = need > 0 ? need : 1;
   kp<<<(int)grid, kBinoWarps * 32, psm, st>>>(p, team_end, wk, (iact || perfo) ? 1 : 0);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_free(e);
   if (iact && p.region.out) {
     binomial_resolve_kernel<<<4 * sms, 256, 0, st>>>(p, team_end, wk.act);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_free(e);
   }
   return cudaFreeAsync(ws, st);
 }
