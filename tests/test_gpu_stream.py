@@ -210,3 +210,39 @@ def test_iact_lane_tables_across_chunks(shape, spec_fn, monkeypatch):
     assert np.array_equal(a[2], b[2])
     if teams * tpt == 512:  # G = the portfolio's 512-option base block: hits every step
         assert a[0].stats["approx_invocations"] > 0
+
+
+@pytest.mark.parametrize("level", ["thread", "warp"])
+def test_iact_hit_threshold_edges(level, monkeypatch):
+    """Hit iff sqrt_rn(ssq) <= thr: the iACT engines test ssq <= thr2 (the
+    largest ssq whose rounded root is <= thr, found on the host) and take
+    square roots only for near-ties. Pairs of options differing in the spot
+    only, thresholds at the rounded distance and one ulp either side: every
+    engine must match the lockstep engine's IEEE sqrt decisions."""
+    rng = np.random.default_rng(3)
+    tpt, ws, ipt = 32, 32, 2
+    teams = 64
+    n = teams * tpt * ipt
+    G = teams * tpt
+    base = E.make_bs_portfolio(G, 9)
+    deltas = rng.uniform(1e-3, 1.0, G)
+    second = base.copy()
+    second[:, 0] += deltas  # step 1 record = step 0 record + delta in S
+    opts = np.concatenate([base, second])
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    dist = np.sqrt((second[:, 0] - base[:, 0]) ** 2)  # what the engines compute (5 dims, 4 zero)
+    for thr in [float(np.median(dist)), float(np.nextafter(np.median(dist), 0)),
+                float(np.nextafter(np.median(dist), 1))]:
+        spec = lambda: E.iact(1, thr, None, level)
+        a = _run(grid, n, d_opts, spec)
+        monkeypatch.setenv("HPAC_IACT_LANE", "0")
+        b = _run(grid, n, d_opts, spec)
+        monkeypatch.delenv("HPAC_IACT_LANE")
+        c = _run(grid, n, d_opts, spec, engine="thread")
+        for r in (b, c):
+            assert np.array_equal(a[2], r[2])
+            assert np.array_equal(a[1], r[1])
+        if level == "thread":
+            want = (dist <= thr).astype(np.uint8)
+            assert np.array_equal(a[2][G:], want)
