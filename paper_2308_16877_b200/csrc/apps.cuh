@@ -535,46 +535,53 @@ struct AppKmeansDmma : AppKmeans {
 // multiply-adds (fma() is exactly rounded on both sides), shared with the
 // oracle, so the contributions (and TAF decisions on them) are bit-identical
 // to the CPU restatement.
-// Coefficients live in constant memory on the device so the DFMAs take them
-// as c[bank][offset] operands (64-bit immediates would otherwise be
-// re-materialised with two integer moves per use inside the pair loop).
-// [0] log2(e), [1] ln2 (rounded: one-FMA reduction, |k| small), [2..12] the
-// degree-11 polynomial a11..a1 (least-squares fit of e^r on |r| <= ln2/2 with
-// a0 = a1 = 1; tools/fit_exp.py), [13] a0, [15] the 1.5*2^52 shifter
-static __constant__ double kLavaExpC[16] = {
-    1.4426950408889634, 0x1.62e42fefa39efp-1, 0x1.af8b4d5192f39p-26,
-    0x1.28ac933b441b4p-22, 0x1.71ddd52442153p-19, 0x1.a0199bbdcc2b9p-16,
-    0x1.a01a01c18b821p-13, 0x1.6c16c18319b74p-10, 0x1.111111110bf92p-7,
-    0x1.5555555551097p-5, 0x1.5555555555569p-3, 0x1.0000000000008p-1,
-    0x1.0000000000000p+0, 1.0, 0.0,
-    0x1.8p52};
+// e^x = 2^k * 2^(j/64) * e^r, n = rint(64 x/ln2) = 64k + j, r = x - n ln2/64
+// (two-constant reduction, |r| <= ln2/128) and e^r by its degree-5 Taylor
+// polynomial (truncation <= 3.5e-17 relative); 2^(j/64) from a 64-entry
+// table (correctly rounded, staged in shared memory by AppLavaMD::init). A
+// fixed sequence of correctly rounded operations and fused multiply-adds, so
+// the oracle's restatement (oracle/hpac_oracle.c lava_exp) is bit-identical.
+// 10 FP64 operations instead of the 14 of a degree-11 polynomial on
+// |r| <= ln2/2, and <= 1.5 ulp instead of 1.2e-15.
+static __constant__ double kLavaExpT[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+#define HPAC_LAVA_L64 0x1.71547652b82fep+6  /* 64/ln2 */
+#define HPAC_LAVA_LN2_64_HI 0x1.62e42fefa39efp-7
+#define HPAC_LAVA_LN2_64_LO 0x1.abc9e3b39803fp-62
+#define HPAC_LAVA_SHIFT 0x1.8p52
 
-__host__ __device__ __forceinline__ double lava_exp(double x) {
-#ifdef __CUDA_ARCH__
-  const double* c = kLavaExpC;
-  // rint(x*log2e) via the 1.5*2^52 shifter on the fused product
-  const double kd = __dsub_rn(fma(x, c[0], c[15]), c[15]);
-#else
-  static const double c[16] = {
-    1.4426950408889634, 0x1.62e42fefa39efp-1, 0x1.af8b4d5192f39p-26,
-    0x1.28ac933b441b4p-22, 0x1.71ddd52442153p-19, 0x1.a0199bbdcc2b9p-16,
-    0x1.a01a01c18b821p-13, 0x1.6c16c18319b74p-10, 0x1.111111110bf92p-7,
-    0x1.5555555551097p-5, 0x1.5555555555569p-3, 0x1.0000000000008p-1,
-    0x1.0000000000000p+0, 1.0, 0.0,
-    0x1.8p52};
-  const double kd = fma(x, c[0], c[15]) - c[15];
-#endif
-  const double r = fma(-kd, c[1], x);
-  double s = c[2];  // a11
-#pragma unroll
-  for (int i = 3; i <= 13; ++i) s = fma(s, r, c[i]);
-  const int k = (int)kd;
-#ifdef __CUDA_ARCH__
+__device__ __forceinline__ double lava_exp(double x, const double* tab) {
+  const double kd = __dsub_rn(fma(x, HPAC_LAVA_L64, HPAC_LAVA_SHIFT), HPAC_LAVA_SHIFT);
+  double r = fma(-kd, HPAC_LAVA_LN2_64_HI, x);
+  r = fma(-kd, HPAC_LAVA_LN2_64_LO, r);
+  double s = 0x1.1111111111111p-7;  // 1/120
+  s = fma(s, r, 0x1.5555555555555p-5);
+  s = fma(s, r, 0x1.5555555555555p-3);
+  s = fma(s, r, 0x1.0000000000000p-1);
+  s = fma(s, r, 1.0);
+  s = fma(s, r, 1.0);
+  const int n = (int)kd;
+  const double t = __dmul_rn(tab[n & 63], s);
+  const int k = n >> 6;  // floor(n / 64)
   // exact power-of-two scaling == ldexp while the result stays normal: add
-  // k to the exponent field (s in [0.7, 1.42]) on the integer pipe
-  if (k > -1021 && k < 1022) return __longlong_as_double(__double_as_longlong(s) + ((long long)k << 52));
-#endif
-  return ldexp(s, k);
+  // k to the exponent field (t in [0.99, 2.01]) on the integer pipe
+  if (k > -1021 && k < 1022) return __longlong_as_double(__double_as_longlong(t) + ((long long)k << 52));
+  return ldexp(t, k);
 }
 
 __host__ __device__ __forceinline__ int lava_neighbours(int64_t box, int b1, int64_t* nb) {
@@ -616,7 +623,7 @@ __host__ __device__ __forceinline__ int64_t lava_neighbour_at(int64_t box, int b
 // engine state live around it (TAF windows, votes): the exact and the
 // approximate kernels run the identical loop.
 static __device__ __noinline__ double4 lava_box_contribution(const double* rv_home, const double* s, int P,
-                                                      double na2) {
+                                                      double na2, const double* etab) {
   const double4 me = *reinterpret_cast<const double4*>(rv_home);
   // exponent argument -a2 (vA + vB - dot) with -a2 folded into the home
   // particle (once) and into the staged vB (staging): 5 ops instead of 6
@@ -633,7 +640,7 @@ static __device__ __noinline__ double4 lava_box_contribution(const double* rv_ho
     const double2 b23 = *reinterpret_cast<const double2*>(s + j * 4 + 2);
     const double q2 = s[P * 4 + j];  // 2*qv, staged (exact doubling)
     const double dotn = fma(azn, b23.y, fma(ayn, b23.x, __dmul_rn(axn, b01.y)));
-    const double vij = lava_exp(__dsub_rn(__dadd_rn(an, b01.x), dotn));  // b01.x = -a2 vB
+    const double vij = lava_exp(__dsub_rn(__dadd_rn(an, b01.x), dotn), etab);  // b01.x = -a2 vB
     // t = 2 q vij exactly as before (power-of-two scaling is exact); the
     // potential is accumulated doubled and halved once at the end: the
     // same bits as summing q*vij
@@ -655,7 +662,11 @@ struct AppLavaMD : AppBase {
   static constexpr bool HAS_IACT = false;  // no region inputs (iACT needs in(...))
   static constexpr int IN_MAX = 1;
   static constexpr int OUT_MAX = 4;
-  __device__ static void init(const EngineParams&, double*) {}
+  // the exp table (lava_exp) after the staged particles: [P*5, P*5 + 64)
+  __device__ static void init(const EngineParams& p, double* scratch) {
+    double* tab = scratch + (size_t)p.region.lavamd_particles * 5;
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) tab[i] = kLavaExpT[i];
+  }
   __device__ static int encounters(const EngineParams& p, int64_t idx) {
     return lava_neighbours(idx, p.region.lavamd_boxes1d, nullptr);
   }
@@ -691,7 +702,7 @@ struct AppLavaMD : AppBase {
                               double (&out)[OUT_MAX], const double* s, int local, int) {
     const int P = p.region.lavamd_particles;
     const double na2 = -__dmul_rn(__dmul_rn(2.0, p.region.lavamd_alpha), p.region.lavamd_alpha);
-    const double4 f = lava_box_contribution(p.region.in + (idx * P + local) * 4, s, P, na2);
+    const double4 f = lava_box_contribution(p.region.in + (idx * P + local) * 4, s, P, na2, s + P * 5);
     out[0] = f.x;
     out[1] = f.y;
     out[2] = f.z;

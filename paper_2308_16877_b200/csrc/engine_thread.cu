@@ -564,7 +564,7 @@ size_t engine_thread_smem(EngineParams& p) {
   p.smem_scratch_off = (int)off;
   if (p.region.app == HPAC_APP_KMEANS && !p.warp_eval)  // centroids + squared norms
     off += (size_t)p.region.kmeans_k * p.region.kmeans_dims + p.region.kmeans_k + 1;
-  if (p.region.app == HPAC_APP_LAVAMD) off += (size_t)p.region.lavamd_particles * 5;
+  if (p.region.app == HPAC_APP_LAVAMD) off += (size_t)p.region.lavamd_particles * 5 + 64;  // + exp table
   p.smem_ctl_off = (int)off;
   // control ints: 16 fixed + generic-ws words (4 per logical warp + 3 per table)
   size_t ctl_ints = 16 + 4 * (size_t)p.wpt + 3 * (size_t)p.wpt * (p.tpw > 0 ? p.tpw : 1) + 4;
