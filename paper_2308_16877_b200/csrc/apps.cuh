@@ -11,6 +11,16 @@
 
 namespace hpac {
 
+// black_scholes_call, bench/blackscholes.hpp:21-36, in its two-erfc form;
+// bs_call's path for infinite spot/strike/vol/maturity. Out of line: never
+// taken on finite inputs, and kept out of the hot path's register allocation.
+static __device__ __noinline__ double bs_call_two_erfc(double spot, double disc_strike, double d1,
+                                                double d2) {
+  const double n1 = 0.5 * fm::erfc(d1 * -0.70710678118654752440);
+  const double n2 = 0.5 * fm::erfc(d2 * -0.70710678118654752440);
+  return spot * n1 - disc_strike * n2;
+}
+
 // black_scholes_call, bench/blackscholes.hpp:21-36. Returns false where the
 // reference throws ConfigError (invalid parameters). The transcendental
 // functions are csrc/fastmath.cuh's (<= 1 ulp exp/log, <= 4 ulp erfc, the
@@ -29,10 +39,24 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
   double d1 = fm::div(fm::log(fm::div(spot, strike)) + (rate + 0.5 * vol * vol) * mat, sst);
   double d2 = d1 - sst;
   // norm_cdf(x) = erfc(-x/sqrt2)/2 (blackscholes.hpp:21); the division by
-  // sqrt2 is a multiplication by -1/sqrt2 here (<= 1 ulp in the argument)
-  double n1 = 0.5 * fm::erfc(d1 * -0.70710678118654752440);
-  double n2 = 0.5 * fm::erfc(d2 * -0.70710678118654752440);
-  price = spot * n1 - disc_strike * n2;
+  // sqrt2 is a multiplication by 1/sqrt2 here (<= 1 ulp in the argument).
+  // erfc(-d/sqrt2) = y or 2 - y with y = e^(-d^2/2) erfcx(|d|/sqrt2), and
+  // S e^(-d1^2/2) = K e^(-rT) e^(-d2^2/2) (d1 sst - sst^2/2 = log(S/K) + rT),
+  // so the second Gaussian factor is a product instead of a second exp:
+  // D N(d2) = D - S e1 erfcx(a2)/2 (d2 > 0) or S e1 erfcx(a2)/2. N(d1) is
+  // bit-equal to the two-erfc form; D N(d2) agrees to a few ulp.
+  // Infinite spot/strike/vol/maturity (S e1 = inf * 0) keep the two-erfc form.
+  if (!((spot * strike) * (vol * mat) < INFINITY)) {
+    price = bs_call_two_erfc(spot, disc_strike, d1, d2);
+    return true;
+  }
+  const double a1 = fmin(fabs(d1) * 0.70710678118654752440, HPAC_FM_ERFC_AMAX);
+  const double a2 = fmin(fabs(d2) * 0.70710678118654752440, HPAC_FM_ERFC_AMAX);
+  const double e1 = fm::exp_neg_sq(a1);
+  const double y1 = e1 * fm::erfcx_core(a1);                   // erfc(|d1|/sqrt2)
+  const double t2 = 0.5 * (spot * (e1 * fm::erfcx_core(a2)));  // D erfc(|d2|/sqrt2) / 2
+  const double n1 = d1 > 0.0 ? 1.0 - 0.5 * y1 : 0.5 * y1;
+  price = spot * n1 - (d2 > 0.0 ? disc_strike - t2 : t2);
   return true;
 }
 

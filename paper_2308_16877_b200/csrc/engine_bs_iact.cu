@@ -388,7 +388,7 @@ constexpr int kLaneChunk = 32;
 #define HPAC_IACT_LANE_MINB 1  // min 256-thread-equivalent blocks (register cap)
 #endif
 #ifndef HPAC_IACT_LANE_PAIR
-#define HPAC_IACT_LANE_PAIR 1  // price two misses per iteration
+#define HPAC_IACT_LANE_PAIR 0  // 1: price two misses per iteration (117 vs 131 us at 0)
 #endif
 template <int LEVEL, int TS>
 __global__ void __launch_bounds__(kIactMaxT, HPAC_IACT_LANE_MINB) bs_iact_lane_kernel(const EngineParams p) {

@@ -1,22 +1,24 @@
-// engine_stream.cu — the streaming variant of the per-thread engine
+// engine_stream.cu — the streaming variants of the per-thread engine
 // (run_region, engine.hpp:132-402, WorkMapping::kPerThread) for
 // single-encounter regions whose accurate path is a pure function of one
 // AoS input record: Blackscholes (bench/blackscholes.hpp:72-92).
 //
 // Same decisions, stats and outputs as engine_thread.cu (and therefore the
-// reference); what changes is how the HBM side is driven:
-//  * the team's input tile of step s+1 (tpt consecutive 40 B records, one
-//    contiguous span) is fetched by ONE thread with a 1-D bulk TMA copy
-//    (cp.async.bulk ... mbarrier::complete_tx) into a double-buffered shared
-//    tile while the team computes step s, so the FP64-bound evaluation never
-//    waits on an HBM round trip;
-//  * a tile is not fetched at all when every active thread of the team is
-//    known to take the approximate path at s+1 (TAF regime with >= 2
-//    predictions left, or a perforation skip) — TAF/perforation then save the
-//    input bytes as well as the flops;
-//  * the team vote is a __syncthreads_count (no shared atomics), the warp
-//    vote a segment-masked __ballot_sync; per-thread counters are 32-bit and
-//    reduced once per thread at the end.
+// reference); two kernels:
+//  * bs_lane_kernel (the default): barrier-free — each thread reads its own
+//    record with read-only loads only when it evaluates, votes are warp
+//    ballots or one __syncthreads_count per step (team level), 64 registers
+//    (32 warps/SM). C1 exact 82 us per 4 M options vs 90 us for the tile
+//    kernel on the same math (profiles/r04_bs_lane_ab.txt).
+//  * bs_stream_kernel (HPAC_STREAM_TMA=1, A/B tests): the team's input tile of
+//    step s+1 (tpt consecutive 40 B records, one contiguous span) is fetched
+//    by ONE thread with a 1-D bulk TMA copy (cp.async.bulk ...
+//    mbarrier::complete_tx) into a double-buffered shared tile while the team
+//    computes step s; a tile is not fetched at all when every active thread
+//    of the team is known to take the approximate path at s+1 (TAF regime
+//    with >= 2 predictions left, or a perforation skip). The team vote is a
+//    __syncthreads_count, the warp vote a segment-masked __ballot_sync.
+// Per-thread counters are 32-bit and reduced once per thread at the end.
 // Eligibility (runtime.cu): per-thread mapping, no encounters, no barrier in
 // evaluate, warp_size | 32, threads_per_team a multiple of 32 and <= 256,
 // technique none / TAF (h <= 8) / perforation.
@@ -338,6 +340,149 @@ __global__ void __launch_bounds__(kStreamMaxT / PAIR, (PAIR == 2 ? 4 : 3))
   }
 }
 
+// Barrier-free variant (the default): every thread loads its own 40 B
+// record with read-only 64-bit loads when it evaluates, and nothing else.
+// Same schedule, decisions, stats and outputs as bs_stream_kernel. The
+// tile staging above wins nothing once the accurate path is the FP64
+// fastmath closed form: a warp's five loads cover 1,280 contiguous bytes, the
+// other resident warps hide the HBM latency, and dropping the two barriers,
+// the mbarrier waits and the double-buffered tile per step frees the
+// registers and issue slots they took. Approximate lanes load nothing (TAF
+// predictions, perforation skips), like the tile version's skipped fetches.
+// Team votes keep one __syncthreads_count per step.
+#ifndef HPAC_LANE_MINB
+#define HPAC_LANE_MINB 4  // 256-thread blocks per SM: <= 64 registers
+#endif
+template <int TECH, int LEVEL, int HREG>
+__global__ void __launch_bounds__(kStreamMaxT, HPAC_LANE_MINB) bs_lane_kernel(const EngineParams p) {
+  const int tpt = p.tpt;
+  const int phys = threadIdx.x;
+  const int team = p.team_begin + (int)blockIdx.x;
+  const int64_t G = p.stride;
+  const int ws = p.ws;
+  const int hw_lane = phys & 31;
+  const int lane = hw_lane % ws;
+  const unsigned seg_mask = ws >= 32 ? 0xffffffffu : (((1u << ws) - 1u) << (hw_lane - lane));
+  const int64_t team_base = (int64_t)team * tpt;
+  const int64_t tid = team_base + phys;
+  const int nsteps = (int)p.steps;
+  // this thread's items: idx = tid + s*G < n for s < my_steps
+  const int64_t rem = p.n - tid;
+  const int my_steps = rem <= 0 ? 0 : (int)(p.steps < (rem - 1) / G + 1 ? p.steps : (rem - 1) / G + 1);
+  const int64_t team_rem = p.n - team_base;  // active threads of the team at step s: team_rem - s*G
+
+  constexpr int HW = HREG > 0 ? HREG : 1;
+  int taf_mode = kTafFilling, taf_rem = 0, taf_count = 0;
+  double win[HW], last = 0.0;
+#pragma unroll
+  for (int i = 0; i < HW; ++i) win[i] = 0.0;
+  int trip = 0;
+  if (TECH == HPAC_TECH_PERFO && (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
+    trip = (int)trip_count(tid, G, p.n, p.steps);
+
+  unsigned c_total = 0, c_approx = 0, c_warp = 0, c_div = 0;
+  bool resident = false, app_error = false;
+  const double* src = p.region.in + tid * kRec;
+  double* dst = p.region.out ? p.region.out + tid : nullptr;
+  uint8_t* path = p.paths ? p.paths + tid : nullptr;
+
+  for (int step = 0; step < nsteps; ++step) {
+    const bool active = step < my_steps;
+    // ---- predicate (engine.hpp:221-251); 1-encounter regions: the
+    // per-thread and herded perforation counters both equal `step`
+    bool pred = false;
+    if (active) {
+      if (TECH == HPAC_TECH_TAF) pred = taf_mode == kTafPredicting;
+      if (TECH == HPAC_TECH_PERFO)
+        pred = perfo_should_skip32(p.perfo_kind, p.perfo_mod, p.perfo_pct, p.perfo_seed, step, trip,
+                                   tid);
+    }
+    bool approx = pred;
+    if (TECH != kTechNoneStream && LEVEL == HPAC_LEVEL_TEAM) {
+      const int yes = __syncthreads_count(active && pred);
+      const int64_t tr = team_rem - (int64_t)step * G;
+      const int cnt = tr <= 0 ? 0 : (tr < tpt ? (int)tr : tpt);
+      approx = 2 * yes > cnt;  // majority_decision over the team's active threads
+    }
+    if (TECH != kTechNoneStream && LEVEL == HPAC_LEVEL_WARP) {
+      const unsigned bv = __ballot_sync(0xffffffffu, active && pred) & seg_mask;
+      const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
+      approx = 2 * __popc(bv) > __popc(ba);
+    }
+    // ---- lane execution (engine.hpp:303-347)
+    if (active) {
+      if (approx) {
+        if (TECH == HPAC_TECH_TAF) {
+          // TafState::emit_approx, taf.hpp:114-117
+          if (dst) __stcs(dst, last);
+          if (taf_mode == kTafPredicting && --taf_rem == 0) {
+            taf_count = 0;
+            taf_mode = kTafFilling;
+          }
+        }
+        // perforation: output untouched
+      } else {
+        double v = 0.0;
+        if (!bs_call(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3), __ldg(src + 4), v))
+          app_error = true;
+        if (dst) __stcs(dst, v);
+        if (TECH == HPAC_TECH_TAF) {
+          // TafState::observe_accurate, taf.hpp:94-108
+#pragma unroll
+          for (int i = 0; i + 1 < HW; ++i) win[i] = win[i + 1];
+          win[HW - 1] = v;
+          if (taf_count < HREG) ++taf_count;
+          last = v;
+          const bool check =
+              (taf_mode == kTafFilling && taf_count == HREG) || taf_mode == kTafChecking;
+          if (taf_mode == kTafPredicting) {
+            if (--taf_rem == 0) {
+              taf_count = 0;
+              taf_mode = kTafFilling;
+            }
+          } else if (check) {
+            if (taf_window_passes<HW>(win, p.taf_thr)) {
+              taf_rem = p.taf_p;
+              taf_mode = kTafPredicting;
+            } else {
+              taf_mode = kTafChecking;
+            }
+          }
+        }
+      }
+      c_total += 1;
+      if (approx) c_approx += 1;
+      if (path) *path = approx ? 1 : 0;
+    }
+    // ---- warp stats (cost.hpp:66-86)
+    const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
+    const unsigned bx = __ballot_sync(0xffffffffu, active && approx) & seg_mask;
+    if (lane == 0 && ba) {
+      resident = true;
+      c_warp += 1;
+      if (bx != 0 && bx != ba) c_div += 1;
+    }
+    src += G * kRec;
+    if (dst) dst += G;
+    if (path) path += G;
+  }
+
+  const unsigned long long s_total = warp_sum_u32(c_total);
+  const unsigned long long s_approx = warp_sum_u32(c_approx);
+  const unsigned long long s_warp = warp_sum_u32(c_warp);
+  const unsigned long long s_div = warp_sum_u32(c_div);
+  const unsigned long long s_res = warp_sum_u32(resident ? 1u : 0u);
+  const unsigned any_err = __ballot_sync(0xffffffffu, app_error);
+  if (hw_lane == 0) {
+    if (s_total) atomicAdd(&p.counters[kCntTotal], s_total);
+    if (s_approx) atomicAdd(&p.counters[kCntApprox], s_approx);
+    if (s_div) atomicAdd(&p.counters[kCntDivergent], s_div);
+    if (s_warp) atomicAdd(&p.counters[kCntWarpSteps], s_warp);
+    if (s_res) atomicAdd(&p.counters[kCntResidentWarps], s_res);
+    if (any_err) atomicAdd(&p.counters[kCntAppError], 1ull);
+  }
+}
+
 bool engine_stream_eligible(const EngineParams& p) {
   if (p.region.app != HPAC_APP_BLACKSCHOLES) return false;
   if (p.per_team || p.has_enc || p.barrier_eval || p.staged) return false;
@@ -360,10 +505,14 @@ static void stream_launch_h(const EngineParams& p, int nblocks, size_t smem, cud
   // registers, so its doubled ILP is paid for with half the resident warps
   const char* pe = getenv("HPAC_STREAM_PAIR");
   const bool pair_on = pe && strcmp(pe, "1") == 0;
+  const char* te = getenv("HPAC_STREAM_TMA");
+  const bool tma_on = te && strcmp(te, "1") == 0;
   if (p.tpt % 64 == 0 && pair_on)
     bs_stream_kernel<TECH, LEVEL, H, 2><<<nblocks, p.tpt / 2, smem, st>>>(p);
-  else
+  else if (tma_on)
     bs_stream_kernel<TECH, LEVEL, H, 1><<<nblocks, p.tpt, smem, st>>>(p);
+  else
+    bs_lane_kernel<TECH, LEVEL, H><<<nblocks, p.tpt, 0, st>>>(p);
 }
 
 template <int TECH, int LEVEL>

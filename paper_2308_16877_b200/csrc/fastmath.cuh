@@ -146,10 +146,8 @@ HPAC_FM_FN double log(double x) {
   return dk * HPAC_FM_LN2_HI_K - ((hfsq - (s * (hfsq + R) + dk * HPAC_FM_LN2_LO_K)) - f);
 }
 
-// complementary error function
-HPAC_FM_FN double erfc(double x) {
-  if (x != x) return x;
-  const double a = fmin(fabs(x), HPAC_FM_ERFC_AMAX);
+// erfcx(a) = e^(a^2) erfc(a) for a in [0, AMAX]
+HPAC_FM_FN double erfcx_core(double a) {
   const double v = a + HPAC_FM_ERFC_K;  // t = (a-K)/(a+K)
   const double w = fma(2.0, a, 1.0);   // 1 + 2a
   const double r = rcp_core(v * w);    // v*w in [4, 1650]: seed range ok
@@ -160,13 +158,23 @@ HPAC_FM_FN double erfc(double x) {
 #pragma unroll
   for (int i = HPAC_FM_ERFC_N - 2; i >= 0; --i) q = fma(q, u, kErfcP[i]);
   const double p = fma(s, q, 1.0);     // P(u) = erfcx(a) (1+2a)
-  const double g = p * (r * v);  // erfcx(a)
-  // exp(-a^2) with a^2 = hi + lo split (exp(-hi-lo) = exp(-hi)(1-lo))
+  return p * (r * v);
+}
+
+// e^(-a^2) for a in [0, AMAX], with a^2 = hi + lo split
+// (exp(-hi-lo) = exp(-hi)(1-lo))
+HPAC_FM_FN double exp_neg_sq(double a) {
   const double hi = a * a;
   const double lo = fma(a, a, -hi);
-  double e = exp_core(-hi);  // a <= 27.5: -hi >= -756.25
-  e = fma(-lo, e, e);
-  const double y = e * g;
+  const double e = exp_core(-hi);  // a <= 27.5: -hi >= -756.25
+  return fma(-lo, e, e);
+}
+
+// complementary error function
+HPAC_FM_FN double erfc(double x) {
+  if (x != x) return x;
+  const double a = fmin(fabs(x), HPAC_FM_ERFC_AMAX);
+  const double y = exp_neg_sq(a) * erfcx_core(a);
   return x < 0.0 ? 2.0 - y : y;
 }
 

@@ -478,7 +478,7 @@ int prepare(const hpac_grid_t* g, int64_t n, int32_t mapping, const hpac_region_
                     (reinterpret_cast<uintptr_t>(r.in) & 15) == 0 && !(km && strcmp(km, "0") == 0);
     }
     pr.smem = engine_thread_smem(p);
-    // streaming variant (bulk-TMA staged inputs) where it applies;
+    // streaming variant (engine_stream.cu: barrier-free lane kernel) where it applies;
     // HPAC_ENGINE=thread forces the generic engine (A/B parity tests)
     const char* force = getenv("HPAC_ENGINE");
     if (engine_stream_eligible(p) && !(force && strcmp(force, "thread") == 0) &&

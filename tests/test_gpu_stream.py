@@ -1,5 +1,5 @@
-"""The streaming per-thread engines (csrc/engine_stream.cu: bulk-TMA staged
-input tiles; csrc/engine_bs_iact.cu: iACT decide-then-price) against the generic per-thread engine (HPAC_ENGINE=thread) and
+"""The streaming per-thread engines (csrc/engine_stream.cu: barrier-free lane
+kernel and bulk-TMA staged input tiles; csrc/engine_bs_iact.cu: iACT decide-then-price) against the generic per-thread engine (HPAC_ENGINE=thread) and
 the oracle, on ragged shapes the C1 grid never exercises: partial last
 tiles (per-thread fallback loads), logical warps narrower than 32, teams of
 32..256 threads, every decision level, TAF and perforation."""
@@ -110,9 +110,11 @@ def test_stream_engine_vs_oracle_ragged(si):
     assert np.array_equal(g_out, o_out)
 
 
-def test_stream_engine_misaligned_input_falls_back():
+@pytest.mark.parametrize("tma", ["0", "1"])
+def test_stream_engine_misaligned_input_falls_back(tma, monkeypatch):
     # a view starting 8 bytes into the buffer defeats the 16-byte bulk-copy
-    # alignment; the engine must take per-thread loads and stay exact
+    # alignment; the tile kernel must take per-thread loads and stay exact
+    monkeypatch.setenv("HPAC_STREAM_TMA", tma)
     n = 32 * 64 * 4
     opts = E.make_bs_portfolio(n + 1, 3)
     buf = torch.from_numpy(np.concatenate([[0.0], opts.reshape(-1)])).cuda()
@@ -155,6 +157,25 @@ def test_paired_stream_kernel_equals_unpaired(shape, si, monkeypatch):
     grid = E.GridConfig(teams, tpt, ws, ipt)
     a = _run(grid, n, d_opts, SPECS[si])
     monkeypatch.setenv("HPAC_STREAM_PAIR", "1")
+    b = _run(grid, n, d_opts, SPECS[si])
+    for f in STAT_FIELDS:
+        assert a[0].stats[f] == b[0].stats[f], f
+    assert np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("si", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
+def test_lane_kernel_equals_tile_kernel(shape, si, monkeypatch):
+    # bs_lane_kernel (default, barrier-free per-thread loads) vs bs_stream_kernel
+    # (HPAC_STREAM_TMA=1, bulk-TMA staged team tiles): identical decisions,
+    # stats, paths and outputs
+    teams, tpt, ws, ipt, n = shape
+    opts = E.make_bs_portfolio(n, 19)
+    d_opts = dev(opts)
+    grid = E.GridConfig(teams, tpt, ws, ipt)
+    a = _run(grid, n, d_opts, SPECS[si])
+    monkeypatch.setenv("HPAC_STREAM_TMA", "1")
     b = _run(grid, n, d_opts, SPECS[si])
     for f in STAT_FIELDS:
         assert a[0].stats[f] == b[0].stats[f], f
