@@ -11,22 +11,16 @@
 
 namespace hpac {
 
-// black_scholes_call, bench/blackscholes.hpp:21-36, in its two-erfc form;
-// bs_call's path for infinite spot/strike/vol/maturity. Out of line: never
-// taken on finite inputs, and kept out of the hot path's register allocation.
-static __device__ __noinline__ double bs_call_two_erfc(double spot, double disc_strike, double d1,
-                                                double d2) {
-  const double n1 = 0.5 * fm::erfc(d1 * -0.70710678118654752440);
-  const double n2 = 0.5 * fm::erfc(d2 * -0.70710678118654752440);
-  return spot * n1 - disc_strike * n2;
-}
-
-// black_scholes_call, bench/blackscholes.hpp:21-36. Returns false where the
-// reference throws ConfigError (invalid parameters). The transcendental
-// functions are csrc/fastmath.cuh's (<= 1 ulp exp/log, <= 4 ulp erfc, the
-// libdevice bounds, at about half libdevice's instruction count).
-__device__ __forceinline__ bool bs_call(double spot, double strike, double rate, double vol,
-                                        double mat, double& price) {
+// black_scholes_call, bench/blackscholes.hpp:21-36, for any arguments.
+// Returns false where the reference throws ConfigError (invalid
+// parameters). The transcendental functions are csrc/fastmath.cuh's (<= 1 ulp
+// exp/log, <= 4 ulp erfc, the libdevice bounds, at about half libdevice's
+// instruction count).
+#ifndef HPAC_BS_GENERAL_ATTR
+#define HPAC_BS_GENERAL_ATTR __forceinline__  // __noinline__: 90.5 vs 78.1 us exact (call ABI spills)
+#endif
+static __device__ HPAC_BS_GENERAL_ATTR bool bs_call_general(double spot, double strike, double rate,
+                                                    double vol, double mat, double& price) {
   if (!(spot > 0) || !(strike > 0) || !(mat > 0) || !(vol >= 0) || !isfinite(rate))
     return false;
   double disc_strike = strike * fm::exp(-rate * mat);
@@ -45,9 +39,12 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
   // so the second Gaussian factor is a product instead of a second exp:
   // D N(d2) = D - S e1 erfcx(a2)/2 (d2 > 0) or S e1 erfcx(a2)/2. N(d1) is
   // bit-equal to the two-erfc form; D N(d2) agrees to a few ulp.
-  // Infinite spot/strike/vol/maturity (S e1 = inf * 0) keep the two-erfc form.
-  if (!((spot * strike) * (vol * mat) < INFINITY)) {
-    price = bs_call_two_erfc(spot, disc_strike, d1, d2);
+  // Infinite spot/strike/vol/maturity (S e1 = inf * 0) and a discounted
+  // strike that overflowed or underflowed (the identity needs 0 < D < inf)
+  // keep the two-erfc form.
+  if (!((spot * strike) * (vol * mat) < INFINITY) || !(disc_strike > 0.0 && disc_strike < INFINITY)) {
+    price = 0.5 * fm::erfc(d1 * -0.70710678118654752440) * spot -
+            disc_strike * (0.5 * fm::erfc(d2 * -0.70710678118654752440));
     return true;
   }
   const double a1 = fmin(fabs(d1) * 0.70710678118654752440, HPAC_FM_ERFC_AMAX);
@@ -55,6 +52,37 @@ __device__ __forceinline__ bool bs_call(double spot, double strike, double rate,
   const double e1 = fm::exp_neg_sq(a1);
   const double y1 = e1 * fm::erfcx_core(a1);                   // erfc(|d1|/sqrt2)
   const double t2 = 0.5 * (spot * (e1 * fm::erfcx_core(a2)));  // D erfc(|d2|/sqrt2) / 2
+  const double n1 = d1 > 0.0 ? 1.0 - 0.5 * y1 : 0.5 * y1;
+  price = spot * n1 - (d2 > 0.0 ? disc_strike - t2 : t2);
+  return true;
+}
+
+// The same function, with the argument checks of every step hoisted into one
+// integer range test: spot, strike in [2^-500, 2^500), vol in [2^-500, 2^8),
+// maturity in [2^-500, 2^5), |rate| < 2^3. Inside that box every check of
+// bs_call_general passes (valid arguments, finite S e1, sst > 0, exp
+// argument within [-256, 256] so 0 < D < inf, divisors and the log argument
+// normal and in the reciprocal seed's range), so the straight-line code below
+// returns the same bits; anything else takes bs_call_general.
+__device__ __forceinline__ bool bs_call(double spot, double strike, double rate, double vol,
+                                        double mat, double& price) {
+  const uint64_t lo = 0x20B0000000000000ull;  // 2^-500
+  const uint64_t bs = (uint64_t)__double_as_longlong(spot), bk = (uint64_t)__double_as_longlong(strike),
+                 bv = (uint64_t)__double_as_longlong(vol), bt = (uint64_t)__double_as_longlong(mat),
+                 br = (uint64_t)__double_as_longlong(rate) & 0x7fffffffffffffffull;
+  const bool fast = bs - lo < 0x5F30000000000000ull - lo && bk - lo < 0x5F30000000000000ull - lo &&
+                    bv - lo < 0x4070000000000000ull - lo && bt - lo < 0x4040000000000000ull - lo &&
+                    br < 0x4020000000000000ull;
+  if (!fast) return bs_call_general(spot, strike, rate, vol, mat, price);
+  const double disc_strike = strike * fm::exp_core(-rate * mat);
+  const double sst = vol * sqrt(mat);
+  const double d1 = fm::div_core(fm::log_core(fm::div_core(spot, strike)) + (rate + 0.5 * vol * vol) * mat, sst);
+  const double d2 = d1 - sst;
+  const double a1 = fmin(fabs(d1) * 0.70710678118654752440, HPAC_FM_ERFC_AMAX);
+  const double a2 = fmin(fabs(d2) * 0.70710678118654752440, HPAC_FM_ERFC_AMAX);
+  const double e1 = fm::exp_neg_sq(a1);
+  const double y1 = e1 * fm::erfcx_core(a1);
+  const double t2 = 0.5 * (spot * (e1 * fm::erfcx_core(a2)));
   const double n1 = d1 > 0.0 ? 1.0 - 0.5 * y1 : 0.5 * y1;
   price = spot * n1 - (d2 > 0.0 ? disc_strike - t2 : t2);
   return true;

@@ -84,13 +84,18 @@ HPAC_FM_FN double rcp_core(double d) {
   return fma(r, fma(e, e, e), r);
 }
 
+// a/b to within 1 ulp for |b| in [2^-1000, 2^1000] (the seed's range)
+HPAC_FM_FN double div_core(double a, double b) {
+  const double r = rcp_core(b);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+
 // a/b to within 1 ulp; IEEE division when b is outside the seed's range
 HPAC_FM_FN double div(double a, double b) {
   const uint32_t eb = ((uint32_t)hi_word(b) >> 20) & 0x7ff;
   if (eb < 0x3ff - 1000 || eb > 0x3ff + 1000) return a / b;
-  const double r = rcp_core(b);
-  const double q = a * r;
-  return fma(fma(-b, q, a), r, q);
+  return div_core(a, b);
 }
 
 // e^y for y in [-756.25, 710] (no NaN): 2^n is applied as two normal
@@ -116,18 +121,9 @@ HPAC_FM_FN double exp(double y) {
   return exp_core(y < -746.0 ? -746.0 : (y > 710.0 ? 710.0 : y));
 }
 
-// natural log (fdlibm decomposition, our own fit of R)
-HPAC_FM_FN double log(double x) {
-  int32_t hx = hi_word(x);
-  int32_t kadj = 0;
-  // one integer test routes zero, negatives, subnormals, inf and NaN aside
-  if (hx < 0x00100000 || hx >= 0x7ff00000) {
-    if (x == 0.0) return -INFINITY;
-    if (!(x > 0.0) || x == INFINITY) return x == INFINITY ? x : NAN;
-    x *= 0x1p54;  // subnormal
-    kadj = -54;
-    hx = hi_word(x);
-  }
+// natural log of a positive normal finite x, with an exponent adjustment
+// (fdlibm decomposition, our own fit of R)
+HPAC_FM_FN double log_reduced(double x, int32_t hx, int32_t kadj) {
   hx += 0x3ff00000 - 0x3fe6a09e;
   const int32_t k = (hx >> 20) - 0x3ff + kadj;
   hx = (hx & 0x000fffff) + 0x3fe6a09e;
@@ -144,6 +140,24 @@ HPAC_FM_FN double log(double x) {
   R *= z;
   const double dk = (double)k;
   return dk * HPAC_FM_LN2_HI_K - ((hfsq - (s * (hfsq + R) + dk * HPAC_FM_LN2_LO_K)) - f);
+}
+
+// natural log of a positive normal finite x
+HPAC_FM_FN double log_core(double x) { return log_reduced(x, hi_word(x), 0); }
+
+// natural log
+HPAC_FM_FN double log(double x) {
+  int32_t hx = hi_word(x);
+  int32_t kadj = 0;
+  // one integer test routes zero, negatives, subnormals, inf and NaN aside
+  if (hx < 0x00100000 || hx >= 0x7ff00000) {
+    if (x == 0.0) return -INFINITY;
+    if (!(x > 0.0) || x == INFINITY) return x == INFINITY ? x : NAN;
+    x *= 0x1p54;  // subnormal
+    kadj = -54;
+    hx = hi_word(x);
+  }
+  return log_reduced(x, hx, kadj);
 }
 
 // erfcx(a) = e^(a^2) erfc(a) for a in [0, AMAX]

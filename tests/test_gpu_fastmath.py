@@ -54,3 +54,40 @@ def test_bs_prices_match_libdevice_formula():
     spot = opts.reshape(n, 5)[:, 0]
     assert np.all(np.isfinite(a))
     assert np.all(np.abs(a - b) <= 1e-13 * spot + 1e-12 * np.abs(b)), np.max(np.abs(a - b))
+
+
+def test_bs_fast_domain_edges_match_libdevice_formula():
+    # apps.cuh bs_call prices inside an integer-tested box (spot, strike in
+    # [2^-500, 2^500), vol < 2^8, maturity < 2^5, |rate| < 2^3) without the
+    # per-step argument checks and falls back to bs_call_general outside it:
+    # options on both sides of every edge, plus log-uniform random ones, agree
+    # with the libdevice formula
+    one_minus = 1.0 - 2.0 ** -52
+    base = np.array([100.0, 95.0, 0.03, 0.2, 1.0])
+    edges = {0: [2.0 ** -500, 2.0 ** -500 * one_minus, 2.0 ** 500 * one_minus, 2.0 ** 500, 1e-160, 1e160],
+             1: [2.0 ** -500, 2.0 ** -500 * one_minus, 2.0 ** 500 * one_minus, 2.0 ** 500, 1e-160, 1e160],
+             2: [-8.0 * one_minus, 8.0 * one_minus, 8.0, -8.0, 20.0, -0.5],
+             3: [2.0 ** -500, 2.0 ** -500 * one_minus, 256.0 * one_minus, 256.0, 300.0, 1e-200],
+             4: [2.0 ** -500, 2.0 ** -500 * one_minus, 32.0 * one_minus, 32.0, 40.0, 1e-200]}
+    rows = []
+    for col, vals in edges.items():
+        for v in vals:
+            r = base.copy()
+            r[col] = v
+            if col == 0:
+                r[1] = v * 0.95
+            rows.append(r)
+    rng = np.random.default_rng(5)
+    m = 1 << 16
+    rnd = np.stack([10.0 ** rng.uniform(-3, 3, m), 10.0 ** rng.uniform(-3, 3, m),
+                    rng.uniform(-20, 20, m), 10.0 ** rng.uniform(-4, 2.6, m),
+                    10.0 ** rng.uniform(-4, 1.7, m)], axis=1)
+    opts = np.concatenate([np.array(rows), rnd])
+    n = len(opts)
+    a, b = fm_eval("bs", opts, n), fm_eval("ld_bs", opts, n)
+    fin = np.isfinite(b)
+    bad = np.isnan(a) != np.isnan(b)
+    assert not bad.any(), (opts[bad][:5], a[bad][:5], b[bad][:5])
+    assert np.array_equal(a[~fin & ~np.isnan(b)], b[~fin & ~np.isnan(b)])
+    tol = 1e-12 * (opts[fin, 0] + np.abs(b[fin])) + 1e-300
+    assert np.all(np.abs(a[fin] - b[fin]) <= tol), np.max(np.abs(a[fin] - b[fin]) / tol)
