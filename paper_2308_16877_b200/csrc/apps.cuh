@@ -616,14 +616,20 @@ static __constant__ double kLavaExpT[64] = {
 #define HPAC_LAVA_LN2_64_HI 0x1.62e42fefa39efp-7
 #define HPAC_LAVA_LN2_64_LO 0x1.abc9e3b39803fp-62
 #define HPAC_LAVA_SHIFT 0x1.8p52
+// the 64-bit constants of lava_exp as a constant-bank array: the DFMAs take
+// them as c[bank][offset] operands. As literals, ptxas rebuilt each one per
+// pair with two UMOV/IMAD.MOV (12 of ~53 warp instructions per pair).
+static __constant__ double kLavaC[6] = {HPAC_LAVA_L64, HPAC_LAVA_LN2_64_HI, HPAC_LAVA_LN2_64_LO,
+                                        0x1.1111111111111p-7, 0x1.5555555555555p-5,
+                                        0x1.5555555555555p-3};
 
 __device__ __forceinline__ double lava_exp(double x, const double* tab) {
-  const double kd = __dsub_rn(fma(x, HPAC_LAVA_L64, HPAC_LAVA_SHIFT), HPAC_LAVA_SHIFT);
-  double r = fma(-kd, HPAC_LAVA_LN2_64_HI, x);
-  r = fma(-kd, HPAC_LAVA_LN2_64_LO, r);
-  double s = 0x1.1111111111111p-7;  // 1/120
-  s = fma(s, r, 0x1.5555555555555p-5);
-  s = fma(s, r, 0x1.5555555555555p-3);
+  const double kd = __dsub_rn(fma(x, kLavaC[0], HPAC_LAVA_SHIFT), HPAC_LAVA_SHIFT);
+  double r = fma(-kd, kLavaC[1], x);
+  r = fma(-kd, kLavaC[2], r);
+  double s = kLavaC[3];  // 1/120
+  s = fma(s, r, kLavaC[4]);
+  s = fma(s, r, kLavaC[5]);
   s = fma(s, r, 0x1.0000000000000p-1);
   s = fma(s, r, 1.0);
   s = fma(s, r, 1.0);
