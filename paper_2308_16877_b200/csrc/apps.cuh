@@ -112,6 +112,7 @@ struct AppBase {
   static constexpr bool HAS_TAF = true, HAS_IACT = true;
   // occupancy hint for the 256-thread engine instantiation (launch bounds)
   static constexpr int MIN_BLOCKS_256 = 1;
+  static constexpr int min_blocks_256(int) { return -1; }  // -1: MIN_BLOCKS_256
   __device__ static int encounters(const EngineParams& p, int64_t idx) {
     return p.region.encounters ? p.region.encounters[idx] : 1;
   }
@@ -717,6 +718,14 @@ struct AppLavaMD : AppBase {
 #define HPAC_LAVA_MINB 3
 #endif
   static constexpr int MIN_BLOCKS_256 = HPAC_LAVA_MINB;
+  // the TAF kernel (4 outputs x h window, votes) runs best at 64 registers
+  // (32 warps/SM): 96.3 vs 102.5 ms at 48^3; exact prefers 80 (93.3 vs 95.8)
+#ifndef HPAC_LAVA_TAF_MINB
+#define HPAC_LAVA_TAF_MINB 4
+#endif
+  static constexpr int min_blocks_256(int tech) {
+    return tech == HPAC_TECH_TAF ? HPAC_LAVA_TAF_MINB : HPAC_LAVA_MINB;
+  }
   static constexpr bool HAS_IACT = false;  // no region inputs (iACT needs in(...))
   static constexpr int IN_MAX = 1;
   static constexpr int OUT_MAX = 4;

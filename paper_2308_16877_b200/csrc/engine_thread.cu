@@ -63,7 +63,10 @@ __device__ __forceinline__ int lava_tile_order(int i, int b1, int T) {
 }
 
 template <class App, int TECH, int HREG, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? App::MIN_BLOCKS_256 : 1) engine_thread_kernel(const EngineParams p) {
+__global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1
+                                       : (App::min_blocks_256(TECH) > 0 ? App::min_blocks_256(TECH)
+                                                                         : App::MIN_BLOCKS_256))
+    engine_thread_kernel(const EngineParams p) {
   extern __shared__ __align__(16) double smem[];
   constexpr int IN_MAX = App::IN_MAX;
   constexpr int OUT_MAX = App::OUT_MAX;
