@@ -22,6 +22,7 @@ CAPTURES = {  # capture name -> bench workload whose timed kernel it is
     "bs_taf": "blackscholes-4M-taf-h5",
     "bs_exact": None,
     "lavamd_taf": "lavamd-64^3-boxes-x-128-taf-warp",
+    "lavamd_exact": None,
     "kmeans_region": "kmeans-lloyd-16M-x-32-x-64-perfo-random-team",
     "kmeans_update": None,
     "kmeans_compact": None,

@@ -37,9 +37,10 @@ cap() {  # name, kernel regex, skip, bench args...   (CAPS=regex: only matching 
 # price kernel (exact arm first: warmup+steps launches, then the iACT arm)
 cap binomial_iact 'binomial_price_kernel' 2 --steps 1 --warmup 1
 cap binomial_exact 'binomial_price_kernel' 0 --steps 1 --warmup 1
-cap bs_taf 'bs_stream_kernel<.int.0' 0 --workload blackscholes --steps 1 --warmup 1
-cap bs_exact 'bs_stream_kernel<.int.3' 0 --workload blackscholes --steps 1 --warmup 1
+cap bs_taf 'bs_lane_kernel<.int.0' 0 --workload blackscholes --steps 1 --warmup 1
+cap bs_exact 'bs_lane_kernel<.int.3' 0 --workload blackscholes --steps 1 --warmup 1
 cap lavamd_taf 'engine_thread_kernel<hpac::AppLavaMD, .int.0' 0 --workload lavamd --steps 1 --warmup 1
+cap lavamd_exact 'engine_thread_kernel<hpac::AppLavaMD, .int.3' 0 --workload lavamd --steps 1 --warmup 1
 # the Lloyd loop runs as a CUDA graph with a conditional node, whose kernel
 # nodes ncu cannot profile: capture the host-driven loop (same kernels)
 export HPAC_KMEANS_HOST_LOOP=1
