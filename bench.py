@@ -779,16 +779,16 @@ def our_arm(args, wl, emit=True):
                 E.run_region_host(grid, n, mapping, hreg, spec)
             e2e_items = job_items
         else:
-            # team-range split: copy the whole portfolio in, run this rank's
-            # teams, copy the whole price array out (every rank moves n_total)
+            # team-range split: each rank's host entry moves only its team
+            # range's options in and prices out (2-D column-block copies,
+            # hpac_run_region_host_teams); all ranks together move the whole
+            # portfolio once per step
             zc = 0
-            e2e_note = "each rank copies the whole global portfolio in and the price array out"
+            e2e_note = ("each rank moves only its team range's options and prices "
+                        "(hpac_run_region_host_teams); bytes are the job's total")
 
             def e2e_step():
-                d_in.copy_(h_in, non_blocking=True)
-                E.run_region(grid, n, mapping, mk(out), spec, stream=stream, team_range=team_range)
-                h_out.copy_(out, non_blocking=True)
-                torch.cuda.synchronize()
+                E.run_region_host(grid, n, mapping, hreg, spec, team_range=team_range)
             e2e_step()
             e2e_items = job_items
         if dist is not None:

@@ -315,6 +315,21 @@ inline LaunchResult run_region_host(const GridConfig& grid, long long n, WorkMap
   return detail::to_result(st);
 }
 
+// One team range [team_begin, team_end) of the grid with host buffers: only
+// the range's items move (the per-rank call of a multi-GPU split).
+inline LaunchResult run_region_host_teams(const GridConfig& grid, long long n, WorkMapping mapping,
+                                          const Region& host_region, const ApproxSpec* spec,
+                                          int team_begin, int team_end) {
+  hpac_grid_t g = grid.c();
+  hpac_stats_t st{};
+  char err[1024];
+  int rc = hpac_run_region_host_teams(&g, n, static_cast<int32_t>(mapping), &host_region.r,
+                                      spec ? &spec->s : nullptr, team_begin, team_end, &st, err,
+                                      sizeof err);
+  detail::check(rc, err, &st);
+  return detail::to_result(st);
+}
+
 // ---- K-Means (bench/kmeans.hpp:62-144) --------------------------------------
 struct KmeansResult {
   int iterations = 0;

@@ -235,6 +235,20 @@ int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
                          const hpac_region_t* host_region, const hpac_spec_t* spec,
                          hpac_stats_t* stats, char* err, size_t errlen);
 
+/* hpac_run_region_host for the logical teams [team_begin, team_end) of the
+   grid only (the multi-GPU split of one global grid, machine.hpp:77-84:
+   each rank runs a contiguous team range with the global stride). The
+   range's items form a column block of the [steps x G] item matrix
+   (per-team: columns [team_begin, team_end) of G = num_teams; per-thread:
+   columns [team_begin, team_end) x threads_per_team of G = num_teams x
+   threads_per_team), so only that block moves each way (2-D copies); items
+   outside it are neither read nor written. Blackscholes and Binomial
+   regions. team_begin = team_end = 0: the whole grid (= hpac_run_region_host). */
+int hpac_run_region_host_teams(const hpac_grid_t* grid, int64_t n, int32_t mapping,
+                               const hpac_region_t* host_region, const hpac_spec_t* spec,
+                               int32_t team_begin, int32_t team_end, hpac_stats_t* stats,
+                               char* err, size_t errlen);
+
 /* Stats of the last asynchronous launch on this thread (after stream sync). */
 int hpac_stats_fetch(hpac_stats_t* stats);
 

@@ -107,6 +107,8 @@ def _declare(lib):
         "hpac_arena_required": (C.c_int, [P(Grid), P(Region), P(Spec), P(C.c_uint64), P(C.c_uint64), C.c_char_p, C.c_size_t]),
         "hpac_run_region": (C.c_int, [P(Grid), C.c_int64, C.c_int32, P(Region), P(Spec), P(Launch), P(Stats), C.c_char_p, C.c_size_t]),
         "hpac_run_region_host": (C.c_int, [P(Grid), C.c_int64, C.c_int32, P(Region), P(Spec), P(Stats), C.c_char_p, C.c_size_t]),
+        "hpac_run_region_host_teams": (C.c_int, [P(Grid), C.c_int64, C.c_int32, P(Region), P(Spec), C.c_int32, C.c_int32,
+                                                 P(Stats), C.c_char_p, C.c_size_t]),
         "hpac_stats_fetch": (C.c_int, [P(Stats)]),
         "hpac_kmeans_run": (C.c_int, [P(Grid), P(KmeansProblem), P(Spec), C.c_void_p, P(KmeansResult), C.c_char_p, C.c_size_t]),
         "hpac_make_bs_portfolio": (C.c_int, [C.c_int64, C.c_uint64, C.c_int32, C.c_double, C.c_void_p]),

@@ -775,11 +775,70 @@ namespace hpac {
 cudaMemPool_t bino_pool() { return ::host_entry_pool(); }
 }  // namespace hpac
 
+namespace {
+// items [c0, c1) of every row of the [rows x G] matrix of `rec`-double
+// records, rows cut at n (the last row may be ragged): one 2-D copy for the
+// whole rows of the block, one 1-D copy for the ragged part
+cudaError_t copy_column_block(double* dst, const double* src, int64_t n, int64_t G, int64_t c0,
+                              int64_t c1, int rec, cudaMemcpyKind kind, cudaStream_t s) {
+  if (c1 <= c0 || n <= c0) return cudaSuccess;
+  const int64_t full = n >= c1 ? (n - c1) / G + 1 : 0;  // rows whose block is entirely < n
+  const size_t pitch = (size_t)G * rec * 8, width = (size_t)(c1 - c0) * rec * 8;
+  cudaError_t e = cudaSuccess;
+  if (full > 0)
+    e = cudaMemcpy2DAsync(dst + (size_t)c0 * rec, pitch, src + (size_t)c0 * rec, pitch, width,
+                          (size_t)full, kind, s);
+  const int64_t r0 = full * G + c0;  // the block's first item in the next row
+  if (e == cudaSuccess && r0 < n) {
+    const int64_t cnt = (n - r0) < (c1 - c0) ? (n - r0) : (c1 - c0);
+    e = cudaMemcpyAsync(dst + (size_t)r0 * rec, src + (size_t)r0 * rec, (size_t)cnt * rec * 8, kind, s);
+  }
+  return e;
+}
+}  // namespace
+
+static int run_region_host_impl(const hpac_grid_t* grid, int64_t n, int32_t mapping,
+                                const hpac_region_t* host_region, const hpac_spec_t* spec,
+                                int32_t team_begin, int32_t team_end, hpac_stats_t* stats,
+                                char* err, size_t el);
+
 // End-to-end entry with host buffers: H2D inputs, run, D2H outputs.
 HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t mapping,
                                   const hpac_region_t* host_region, const hpac_spec_t* spec,
                                   hpac_stats_t* stats, char* err, size_t el) {
+  return run_region_host_impl(grid, n, mapping, host_region, spec, 0, 0, stats, err, el);
+}
+
+// The same for one team range: only its column block of items moves.
+HPAC_API int hpac_run_region_host_teams(const hpac_grid_t* grid, int64_t n, int32_t mapping,
+                                        const hpac_region_t* host_region, const hpac_spec_t* spec,
+                                        int32_t team_begin, int32_t team_end, hpac_stats_t* stats,
+                                        char* err, size_t el) {
+  return run_region_host_impl(grid, n, mapping, host_region, spec, team_begin, team_end, stats,
+                              err, el);
+}
+
+static int run_region_host_impl(const hpac_grid_t* grid, int64_t n, int32_t mapping,
+                                const hpac_region_t* host_region, const hpac_spec_t* spec,
+                                int32_t team_begin, int32_t team_end, hpac_stats_t* stats,
+                                char* err, size_t el) {
   if (!host_region) return fail(err, el, HPAC_ERR_CONFIG, "region is null");
+  const bool ranged = team_begin != 0 || team_end != 0;
+  int64_t col0 = 0, col1 = 0, colG = 0;  // the range's column block (ranged only)
+  if (ranged) {
+    int vr = validate_grid(grid, err, el);
+    if (vr) return vr;
+    if (host_region->app != HPAC_APP_BLACKSCHOLES && host_region->app != HPAC_APP_BINOMIAL)
+      return fail(err, el, HPAC_ERR_UNSUPPORTED,
+                  "team-range host entry: Blackscholes and Binomial regions only");
+    if (team_begin < 0 || team_end > grid->num_teams || team_begin > team_end)
+      return fail(err, el, HPAC_ERR_CONFIG, "team range [%d, %d) outside [0, %d)", team_begin,
+                  team_end, grid->num_teams);
+    const int64_t w = mapping == HPAC_MAP_PER_TEAM ? 1 : grid->threads_per_team;
+    col0 = team_begin * w;
+    col1 = team_end * w;
+    colG = (int64_t)grid->num_teams * w;
+  }
   hpac_region_t r = *host_region;
   int rc = bind_region(&r, err, el);
   if (rc) return rc;
@@ -857,7 +916,7 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
     d.labels = (int32_t*)pinned_device_ptr(r.labels);
     d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true, "centroids");  // read per CTA: stage
   } else {
-    d.in = (const double*)dalloc(in_bytes, r.in, true, "inputs");
+    d.in = (const double*)dalloc(in_bytes, r.in, !ranged, "inputs");
     d.table_out = (const double*)dalloc(tab_bytes, r.table_out, true, "table_out");
     d.encounters = (const int32_t*)dalloc(enc_bytes, r.encounters, true, "encounters");
     // outputs start from the caller's contents where an item can be left
@@ -865,7 +924,17 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
     // the option regions otherwise write every item, so nothing is copied in
     const bool keeps = (spec && spec->technique == HPAC_TECH_PERFO) ||
                        !(r.app == HPAC_APP_BLACKSCHOLES || r.app == HPAC_APP_BINOMIAL);
-    d.out = (double*)dalloc(out_bytes, r.out, keeps, "outputs");
+    d.out = (double*)dalloc(out_bytes, r.out, keeps && !ranged, "outputs");
+    if (ranged && alloc_e == cudaSuccess) {  // the range's column block only
+      cudaError_t ce = copy_column_block(const_cast<double*>(d.in), r.in, n, colG, col0, col1, 5,
+                                         cudaMemcpyHostToDevice, st);
+      if (ce == cudaSuccess && keeps && d.out)
+        ce = copy_column_block(d.out, r.out, n, colG, col0, col1, 1, cudaMemcpyHostToDevice, st);
+      if (ce != cudaSuccess) {
+        alloc_e = ce;
+        alloc_what = "the team range's inputs";
+      }
+    }
     d.centroids = (const double*)dalloc(cen_bytes, r.centroids, true, "centroids");
     d.labels = (int32_t*)dalloc(lab_bytes, r.labels, true, "labels");
   }
@@ -878,13 +947,19 @@ HPAC_API int hpac_run_region_host(const hpac_grid_t* grid, int64_t n, int32_t ma
   hpac_launch_t L{};
   L.stream = st;
   L.synchronous = 1;
+  L.team_begin = team_begin;
+  L.team_end = team_end;
   g_force_thread_engine = zero_copy;
   rc = hpac_run_region(grid, n, mapping, &d, spec, &L, stats, err, el);
   g_force_thread_engine = false;
   if (stats) stats->zero_copy = zero_copy ? 1 : 0;
   if (rc == HPAC_OK && !zero_copy) {
-    if (out_bytes && (e = cudaMemcpyAsync(r.out, d.out, out_bytes, cudaMemcpyDeviceToHost, st)) !=
-                         cudaSuccess)
+    if (out_bytes && ranged &&
+        (e = copy_column_block(r.out, d.out, n, colG, col0, col1, 1, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess)
+      rc = cuda_fail(err, el, e, "copying outputs to the host");
+    if (out_bytes && !ranged &&
+        (e = cudaMemcpyAsync(r.out, d.out, out_bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
       rc = cuda_fail(err, el, e, "copying outputs to the host");
     if (rc == HPAC_OK && lab_bytes &&
         (e = cudaMemcpyAsync(r.labels, d.labels, lab_bytes, cudaMemcpyDeviceToHost, st)) !=

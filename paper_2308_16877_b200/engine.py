@@ -320,13 +320,22 @@ def run_region(grid: GridConfig, n: int, mapping: int, region: Region, spec=None
     return LaunchResult(st.as_dict(), st.kernel_ms)
 
 
-def run_region_host(grid: GridConfig, n: int, mapping: int, region: Region, spec=None) -> LaunchResult:
-    """Same call with host (numpy) buffers: H2D, run, D2H inside."""
+def run_region_host(grid: GridConfig, n: int, mapping: int, region: Region, spec=None,
+                    team_range=None) -> LaunchResult:
+    """Same call with host (numpy) buffers: H2D, run, D2H inside. team_range =
+    (begin, end): only those logical teams run, and only their items move
+    (hpac_run_region_host_teams; Blackscholes and Binomial)."""
     st = abi.Stats()
     err = C.create_string_buffer(1024)
-    rc = abi.lib().hpac_run_region_host(C.byref(grid.c()), n, mapping, C.byref(region.c()),
-                                        C.byref(spec) if spec is not None else None,
-                                        C.byref(st), err, 1024)
+    if team_range is not None:
+        rc = abi.lib().hpac_run_region_host_teams(C.byref(grid.c()), n, mapping, C.byref(region.c()),
+                                                  C.byref(spec) if spec is not None else None,
+                                                  int(team_range[0]), int(team_range[1]),
+                                                  C.byref(st), err, 1024)
+    else:
+        rc = abi.lib().hpac_run_region_host(C.byref(grid.c()), n, mapping, C.byref(region.c()),
+                                            C.byref(spec) if spec is not None else None,
+                                            C.byref(st), err, 1024)
     if rc:
         _raise(rc, err, st)
     return LaunchResult(st.as_dict(), st.kernel_ms)

@@ -88,3 +88,61 @@ def test_binomial_host_entry_outputs(spec_fn, keeps):
     assert np.array_equal(out, d_out.cpu().numpy())
     assert r.stats["approx_invocations"] == rd.stats["approx_invocations"]
     assert bool((out == -7.0).any()) == keeps
+
+
+STATS = ["total_invocations", "approx_invocations", "divergent_warp_steps", "total_warp_steps",
+         "resident_warps", "lattice_nodes"]
+
+
+@pytest.mark.parametrize("app", ["binomial", "blackscholes"])
+@pytest.mark.parametrize("spec_fn", [lambda: None, lambda: E.iact(4, 0.4, level="team"),
+                                     lambda: E.taf(3, 2, 0.3, level="team"), lambda: E.perfo("small", 3)])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_entry_team_ranges(app, spec_fn, pinned):
+    # hpac_run_region_host_teams: the team ranges of one global grid, each
+    # moving only its column block of items, compose to one device launch
+    # (prices, paths of untouched items, summed stats); items outside a
+    # range are neither read nor written
+    if app == "binomial":
+        grid, mp = E.resolve_grid("binomial", 41 * 20, items_per_thread=20)
+        n = grid.num_teams * 20 - 17
+        opts = E.make_binomial_portfolio(n, 21)
+        mk = lambda i, o: E.binomial_region(i, 64, o)
+    else:
+        grid, mp = E.resolve_grid("blackscholes", 37 * 64 * 5, items_per_thread=5)
+        n = grid.num_teams * grid.threads_per_team * 5 - 29
+        opts = E.make_bs_portfolio(n, 21)
+        mk = lambda i, o: E.blackscholes_region(i, o)
+    d_out = torch.full((n,), -7.0, dtype=torch.float64, device="cuda")
+    rd = E.run_region(grid, n, mp, mk(torch.from_numpy(opts).cuda(), d_out), spec_fn())
+    h_in = torch.from_numpy(opts)
+    h_out = torch.full((n,), -7.0, dtype=torch.float64)
+    if pinned:
+        h_in, h_out = h_in.pin_memory(), h_out.pin_memory()
+    T = grid.num_teams
+    cuts = [0, T // 3, T // 3 + 1, (2 * T) // 3, T]
+    tot = {f: 0 for f in STATS}
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        r = E.run_region_host(grid, n, mp, mk(h_in.numpy(), h_out.numpy()), spec_fn(), team_range=(a, b))
+        for f in STATS:
+            tot[f] += r.stats[f]
+        if a == 0:  # after the first range only its items changed
+            got = h_out.numpy().copy()
+            w = 1 if app == "binomial" else grid.threads_per_team
+            G = T * w
+            col = np.arange(n) % G
+            inside = (col >= a * w) & (col < b * w)
+            assert np.array_equal(got[inside], d_out.cpu().numpy()[inside])
+            assert np.all(got[~inside] == -7.0)
+    assert np.array_equal(h_out.numpy(), d_out.cpu().numpy())
+    for f in STATS:
+        assert tot[f] == rd.stats[f], f
+
+
+def test_host_entry_team_range_rejects_other_regions():
+    n, d, k = 64 * 4 * 4, 32, 8
+    pts = E.make_blobs(n, d, k, 7, 8.0)
+    grid, mp = E.resolve_grid("kmeans", n, items_per_thread=4)
+    with pytest.raises(E.UnsupportedError):
+        E.run_region_host(grid, n, mp, E.kmeans_region(pts, pts[:k].copy(), np.zeros(n, np.int32)),
+                          None, team_range=(0, 1))
