@@ -32,6 +32,7 @@
 namespace hpac {
 
 constexpr int kUpdWarps = 4;
+constexpr int kMaxSubsPerWarp = 8;  // kmeans_update_partial: the pipelined stream's sub-chunk table
 
 __global__ void kmeans_forgy(const double* pts, int64_t n, int dims, int k, double* cent) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k * dims; i += gridDim.x * blockDim.x) {
@@ -57,7 +58,8 @@ constexpr int kCompactU = 4;
 __global__ void __launch_bounds__(256)
     kmeans_changed_compact(const int32_t* __restrict__ dist_label, int32_t* __restrict__ assign,
                            int64_t n, int64_t sub, int64_t nsub, int32_t* __restrict__ list,
-                           int32_t* __restrict__ oldlab, int32_t* __restrict__ list_len) {
+                           int32_t* __restrict__ oldlab, int32_t* __restrict__ newlab,
+                           int32_t* __restrict__ list_len) {
   const int lane = threadIdx.x & 31;
   const int64_t gs = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gs >= nsub) return;
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(256)
         const int pos = cnt + __popc(m & ((1u << lane) - 1u));
         list[lo + pos] = (int32_t)(i - lo);
         oldlab[lo + pos] = ol[u];
+        newlab[lo + pos] = nl[u];
         assign[i] = nl[u];
       }
       cnt += __popc(m);
@@ -104,8 +107,9 @@ constexpr int kBatch = 32;
 __global__ void __launch_bounds__(kUpdWarps * 32, 2)
     kmeans_update_partial(const double* __restrict__ pts, const int32_t* __restrict__ dist_label,
                           const int32_t* __restrict__ list, const int32_t* __restrict__ oldlab,
-                          const int32_t* __restrict__ list_len, int64_t sub, int subs_per_warp,
-                          int64_t nsub, int dims, int k, double* __restrict__ part) {
+                          const int32_t* __restrict__ newlab, const int32_t* __restrict__ list_len,
+                          int64_t sub, int subs_per_warp, int64_t nsub, int dims, int k,
+                          double* __restrict__ part) {
   extern __shared__ __align__(16) double acc[];  // [warps][k*dims] then int counts [warps][k]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int kd = k * dims;
@@ -117,58 +121,100 @@ __global__ void __launch_bounds__(kUpdWarps * 32, 2)
   const int64_t gw = (int64_t)blockIdx.x * kUpdWarps + w;
   unsigned long long changed = 0;
   const bool dl = lane < dims;
-  for (int64_t gs = gw * subs_per_warp; gs < (gw + 1) * subs_per_warp && gs < nsub; ++gs) {
-    const int64_t lo = gs * sub;
-    const int len = list_len[gs];
-    changed += len;
-    // lane j of group e0: entry e0 + j (point, new label, old label)
-    auto entry = [&](int e0, int64_t& pi, int& nl, int& ol) {
-      const bool v = e0 + lane < len;
-      pi = v ? lo + list[lo + e0 + lane] : 0;
-      nl = v ? dist_label[pi] : 0;
-      ol = v ? oldlab[lo + e0 + lane] : -1;
-    };
-    if (dims <= 32) {
-      double xa[kBatch], xb[kBatch];
-      int64_t pa = 0, pb = 0;
-      int na = 0, oa = -1, nb = 0, ob = -1;
-      auto fetch = [&](int e0, double (&x)[kBatch], int64_t& pi, int& nl, int& ol) {
-        entry(e0, pi, nl, ol);
-        const int c = len - e0 < kBatch ? len - e0 : kBatch;
+  const int64_t gs0 = gw * subs_per_warp;
+  const int S = gs0 >= nsub ? 0 : (int)(nsub - gs0 < subs_per_warp ? nsub - gs0 : subs_per_warp);
+  if (dims <= 32 && subs_per_warp <= kMaxSubsPerWarp) {
+    // The warp's sub-chunks as ONE stream of entries (sub order, then list
+    // order: the same point order as sub by sub) in batches of 32, software
+    // pipelined two batches deep: batch b+2's entries (index, old and new
+    // label: coalesced loads, no dependent gather) and batch b+1's rows are
+    // in flight while batch b accumulates, so a sub-chunk boundary costs no
+    // memory round trip.
+    const int mylen = lane < S ? list_len[gs0 + lane] : 0;
+    int incl = mylen;
 #pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-          const int64_t pj = __shfl_sync(0xffffffffu, pi, j);
-          x[j] = (j < c && dl) ? __ldcs(pts + pj * dims + lane) : 0.0;
-        }
-      };
-      if (len > 0) fetch(0, xa, pa, na, oa);
-      for (int e0 = 0; e0 < len; e0 += kBatch) {
-        const int c = len - e0 < kBatch ? len - e0 : kBatch;
-        if (e0 + kBatch < len) fetch(e0 + kBatch, xb, pb, nb, ob);
-        if (lane < c) {
-          atomicAdd(&cnts[na], 1);
-          if (oa >= 0) atomicSub(&cnts[oa], 1);
-        }
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int excl[kMaxSubsPerWarp];
 #pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-          if (j >= c) break;
-          const int cn = __shfl_sync(0xffffffffu, na, j), co = __shfl_sync(0xffffffffu, oa, j);
-          if (dl) {
-            my[(size_t)cn * dims + lane] += xa[j];
-            if (co >= 0) my[(size_t)co * dims + lane] -= xa[j];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) xa[j] = xb[j];
-        pa = pb;
-        na = nb;
-        oa = ob;
+    for (int t = 0; t < kMaxSubsPerWarp; ++t) excl[t] = __shfl_sync(0xffffffffu, incl - mylen, t);
+    changed = total;
+    // entry q of the stream: its sub-chunk and list position, its point
+    auto entry = [&](int q, int64_t& pi, int& nl, int& ol) {
+      if (q >= total) {
+        pi = 0;
+        nl = 0;
+        ol = -1;
+        return;
       }
-    } else {
+      int t = 0, et = 0;  // excl[0] = 0 (registers only: no dynamic index)
+#pragma unroll
+      for (int u = 1; u < kMaxSubsPerWarp; ++u)
+        if (u < S && excl[u] <= q) {
+          t = u;
+          et = excl[u];
+        }
+      const int64_t lo = (gs0 + t) * sub;
+      const int64_t at = lo + (q - et);
+      pi = lo + list[at];
+      nl = newlab[at];
+      ol = oldlab[at];
+    };
+    auto rows = [&](int q0, const int64_t pi, double (&x)[kBatch]) {
+      const int c = total - q0 < kBatch ? total - q0 : kBatch;
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const int64_t pj = __shfl_sync(0xffffffffu, pi, j);
+        x[j] = (j < c && dl) ? __ldcs(pts + pj * dims + lane) : 0.0;
+      }
+    };
+    double xa[kBatch], xb[kBatch];
+    int64_t p0 = 0, p1 = 0, p2 = 0;
+    int n0 = 0, o0 = -1, n1 = 0, o1 = -1, n2 = 0, o2 = -1;
+    if (total > 0) {
+      entry(lane, p0, n0, o0);
+      rows(0, p0, xa);
+      entry(kBatch + lane, p1, n1, o1);
+    }
+    for (int q0 = 0; q0 < total; q0 += kBatch) {
+      const int c = total - q0 < kBatch ? total - q0 : kBatch;
+      if (q0 + kBatch < total) rows(q0 + kBatch, p1, xb);
+      if (q0 + 2 * kBatch < total) entry(q0 + 2 * kBatch + lane, p2, n2, o2);
+      if (lane < c) {
+        atomicAdd(&cnts[n0], 1);
+        if (o0 >= 0) atomicSub(&cnts[o0], 1);
+      }
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        if (j >= c) break;
+        const int cn = __shfl_sync(0xffffffffu, n0, j), co = __shfl_sync(0xffffffffu, o0, j);
+        if (dl) {
+          my[(size_t)cn * dims + lane] += xa[j];
+          if (co >= 0) my[(size_t)co * dims + lane] -= xa[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) xa[j] = xb[j];
+      p0 = p1;
+      n0 = n1;
+      o0 = o1;
+      p1 = p2;
+      n1 = n2;
+      o1 = o2;
+    }
+  } else {
+    for (int64_t gs = gs0; gs < gs0 + S; ++gs) {
+      const int64_t lo = gs * sub;
+      const int len = list_len[gs];
+      changed += len;
       for (int e0 = 0; e0 < len; e0 += 32) {
-        int64_t pi;
-        int nl, ol;
-        entry(e0, pi, nl, ol);
+        const bool v = e0 + lane < len;
+        const int64_t pi = v ? lo + list[lo + e0 + lane] : 0;
+        const int nl = v ? newlab[lo + e0 + lane] : 0;
+        const int ol = v ? oldlab[lo + e0 + lane] : -1;
         const int c = len - e0 < 32 ? len - e0 : 32;
         if (lane < c) {
           atomicAdd(&cnts[nl], 1);
@@ -353,7 +399,7 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
   constexpr int kSubsPerWarp = 8;
   const int64_t nsub = warps * kSubsPerWarp;
   const int64_t sub = n > 0 ? (n + nsub - 1) / nsub : 1;
-  int32_t *list = nullptr, *oldlab = nullptr, *list_len = nullptr;
+  int32_t *list = nullptr, *oldlab = nullptr, *newlab = nullptr, *list_len = nullptr;
   auto cleanup = [&]() {
     if (dist_label) cudaFreeAsync(dist_label, st);
     if (part) cudaFreeAsync(part, st);
@@ -361,6 +407,7 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     if (tot) cudaFreeAsync(tot, st);
     if (list) cudaFreeAsync(list, st);
     if (oldlab) cudaFreeAsync(oldlab, st);
+    if (newlab) cudaFreeAsync(newlab, st);
     if (list_len) cudaFreeAsync(list_len, st);
   };
   // run-scoped buffers from the library's retained stream-ordered pool (no
@@ -376,6 +423,7 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
       (!red && (e = palloc(&red, sizeof(double) * (stride + 1)))) ||
       (e = palloc(&tot, sizeof(double) * stride)) || (e = palloc(&list, sizeof(int32_t) * nn)) ||
       (e = palloc(&oldlab, sizeof(int32_t) * nn)) ||
+      (e = palloc(&newlab, sizeof(int32_t) * nn)) ||
       (e = palloc(&list_len, sizeof(int32_t) * (size_t)nsub)) ||
       (e = cudaMemsetAsync(tot, 0, sizeof(double) * stride, st))) {
     cleanup();
@@ -459,9 +507,9 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     ge = region_launch(hreg, cs);
     loop_after_region<<<1, 1, 0, cs>>>(ds);
     kmeans_changed_compact<<<(int)((nsub + 7) / 8), 256, 0, cs>>>(
-        dist_label, pb->assignments, n, sub, nsub, list, oldlab, list_len);
+        dist_label, pb->assignments, n, sub, nsub, list, oldlab, newlab, list_len);
     kmeans_update_partial<<<nparts, kUpdWarps * 32, upd_smem, cs>>>(
-        pb->points, dist_label, list, oldlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
+        pb->points, dist_label, list, oldlab, newlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
     kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, cs>>>(part, nparts,
                                                                               (int)(stride + 1), red);
     int hook_rc = pb->allreduce ? pb->allreduce(red, (int64_t)(stride + 1), pb->allreduce_user, cs)
@@ -548,9 +596,9 @@ HPAC_API int hpac_kmeans_run(const hpac_grid_t* grid, const hpac_kmeans_problem_
     // reference sums all points in order, kmeans.hpp:135-141)
     cudaEventRecord(e0, st);
     kmeans_changed_compact<<<(int)((nsub + 7) / 8), 256, 0, st>>>(
-        dist_label, pb->assignments, n, sub, nsub, list, oldlab, list_len);
+        dist_label, pb->assignments, n, sub, nsub, list, oldlab, newlab, list_len);
     kmeans_update_partial<<<nparts, kUpdWarps * 32, upd_smem, st>>>(
-        pb->points, dist_label, list, oldlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
+        pb->points, dist_label, list, oldlab, newlab, list_len, sub, kSubsPerWarp, nsub, dims, k, part);
     kmeans_reduce_partials<<<(int)((stride + 1 + 255) / 256), 256, 0, st>>>(part, nparts,
                                                                               (int)(stride + 1), red);
     if ((e = cudaGetLastError()) != cudaSuccess) {
