@@ -187,13 +187,35 @@ __global__ void __launch_bounds__(kUpdWarps * 32, 2)
         atomicAdd(&cnts[n0], 1);
         if (o0 >= 0) atomicSub(&cnts[o0], 1);
       }
+      // rows j and j+1 touching four different clusters (the common case)
+      // read all their sums before writing any: two read-modify-write
+      // chains in flight instead of one; a shared cluster keeps the order
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
+      for (int j = 0; j < kBatch; j += 2) {
         if (j >= c) break;
-        const int cn = __shfl_sync(0xffffffffu, n0, j), co = __shfl_sync(0xffffffffu, o0, j);
+        const int ca = __shfl_sync(0xffffffffu, n0, j), oa = __shfl_sync(0xffffffffu, o0, j);
+        const int cb = __shfl_sync(0xffffffffu, n0, j + 1), ob = __shfl_sync(0xffffffffu, o0, j + 1);
+        const bool two = j + 1 < c;
+        const bool apart = two && cb != ca && cb != oa && (ob < 0 || (ob != ca && ob != oa));
         if (dl) {
-          my[(size_t)cn * dims + lane] += xa[j];
-          if (co >= 0) my[(size_t)co * dims + lane] -= xa[j];
+          double* pa = my + (size_t)ca * dims + lane;
+          double* qa = my + (size_t)(oa >= 0 ? oa : 0) * dims + lane;
+          if (apart) {
+            double* pb = my + (size_t)cb * dims + lane;
+            double* qb = my + (size_t)(ob >= 0 ? ob : 0) * dims + lane;
+            const double va = *pa, wa = oa >= 0 ? *qa : 0.0, vb = *pb, wb = ob >= 0 ? *qb : 0.0;
+            *pa = va + xa[j];
+            if (oa >= 0) *qa = wa - xa[j];
+            *pb = vb + xa[j + 1];
+            if (ob >= 0) *qb = wb - xa[j + 1];
+          } else {
+            *pa += xa[j];
+            if (oa >= 0) *qa -= xa[j];
+            if (two) {
+              my[(size_t)cb * dims + lane] += xa[j + 1];
+              if (ob >= 0) my[(size_t)ob * dims + lane] -= xa[j + 1];
+            }
+          }
         }
       }
 #pragma unroll
