@@ -337,6 +337,26 @@ static void lavamd_levels() {  // extension: TAF at warp vs team, staging outsid
   CHECK(threw);
 }
 
+static void host_team_ranges() {  // multi-GPU split with host buffers (hpac_run_region_host_teams)
+  const long long n = 40 * 16 - 9;
+  std::vector<double> opts(n * 5);
+  hpac_make_binomial_portfolio(n, 5, 0.002, opts.data());
+  GridConfig g = grid_of(40, 64, 32, 16);
+  ApproxSpec s = parse_directive("memo(in:4:0.4) level(team) in(o[i:5]) out(p[i])");
+  std::vector<double> whole(n, -1.0), parts(n, -1.0);
+  auto rw = run_region_host(g, n, WorkMapping::kPerTeam, binomial_region(opts.data(), 64, whole.data()), &s);
+  unsigned long long approx = 0, total = 0;
+  for (int a = 0; a < 40; a += 13) {
+    const int b = a + 13 < 40 ? a + 13 : 40;
+    auto r = run_region_host_teams(g, n, WorkMapping::kPerTeam,
+                                   binomial_region(opts.data(), 64, parts.data()), &s, a, b);
+    approx += r.stats.approx_invocations;
+    total += r.stats.total_invocations;
+  }
+  CHECK(parts == whole);
+  CHECK(approx == rw.stats.approx_invocations && total == rw.stats.total_invocations);
+}
+
 int main() {
   std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"baseline_accurate", baseline_accurate}, {"taf_threshold_zero_noise", taf_threshold_zero_noise},
@@ -347,7 +367,8 @@ int main() {
       {"team_vote_multiples", team_vote_multiples}, {"tail_masking", tail_masking},
       {"per_team_mapping", per_team_mapping}, {"arena_overflow", arena_overflow},
       {"deterministic", deterministic}, {"directives_and_grid", directives_and_grid},
-      {"kmeans_small", kmeans_small}, {"lavamd_levels", lavamd_levels}};
+      {"kmeans_small", kmeans_small}, {"lavamd_levels", lavamd_levels},
+      {"host_team_ranges", host_team_ranges}};
   for (auto& [name, fn] : cases) {
     int before = g_fail;
     try {
