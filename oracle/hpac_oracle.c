@@ -512,7 +512,7 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
       lava_neighbours(idx, r->lavamd_boxes1d, nb);
       const int64_t b = nb[round];
       const double* me = r->in + (idx * P + lane) * 4;
-      double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+      double fv = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
       for (int j = 0; j < P; ++j) {
         const double* o2 = r->in + (b * P + j) * 4;
         const double q = r->table_out[b * P + j];
@@ -525,14 +525,17 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
         const double qv = q * vij;
         const double t = qv + qv;
         fv = fv + qv;
-        fx = fma(t, me[1] - o2[1], fx);
-        fy = fma(t, me[2] - o2[2], fy);
-        fz = fma(t, me[3] - o2[3], fz);
+        /* sum_j t (rA - rB) = rA sum_j t - sum_j t rB (apps.cuh
+           lava_box_contribution): one FMA per component and pair */
+        sx = fma(t, o2[1], sx);
+        sy = fma(t, o2[2], sy);
+        sz = fma(t, o2[3], sz);
       }
+      const double f2 = fv + fv; /* sum_j t, exact */
       out[0] = fv;
-      out[1] = fx;
-      out[2] = fy;
-      out[3] = fz;
+      out[1] = fma(me[1], f2, -sx);
+      out[2] = fma(me[2], f2, -sy);
+      out[3] = fma(me[3], f2, -sz);
       return 0;
     }
     case HPAC_APP_TABLE:

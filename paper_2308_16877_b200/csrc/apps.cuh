@@ -688,7 +688,7 @@ static __device__ __noinline__ double4 lava_box_contribution(const double* rv_ho
   // particle (once) and into the staged vB (staging): 5 ops instead of 6
   const double an = __dmul_rn(na2, me.x), axn = __dmul_rn(na2, me.y), ayn = __dmul_rn(na2, me.z),
                azn = __dmul_rn(na2, me.w);
-  double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+  double fv = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
 #ifndef HPAC_LAVA_UNROLL
 #define HPAC_LAVA_UNROLL 1  // measured: 1 (32.7 ms) < 4 (35.5) < 2 (36.5) at 32^3
 #endif
@@ -705,11 +705,13 @@ static __device__ __noinline__ double4 lava_box_contribution(const double* rv_ho
     // same bits as summing q*vij
     const double t = __dmul_rn(q2, vij);
     fv = __dadd_rn(fv, t);
-    fx = fma(t, __dsub_rn(me.y, b01.y), fx);
-    fy = fma(t, __dsub_rn(me.z, b23.x), fy);
-    fz = fma(t, __dsub_rn(me.w, b23.y), fz);
+    // sum_j t (rA - rB) = rA sum_j t - sum_j t rB: one FMA per component
+    // and pair instead of a subtraction and an FMA
+    sx = fma(t, b01.y, sx);
+    sy = fma(t, b23.x, sy);
+    sz = fma(t, b23.y, sz);
   }
-  return make_double4(0.5 * fv, fx, fy, fz);
+  return make_double4(0.5 * fv, fma(me.y, fv, -sx), fma(me.z, fv, -sy), fma(me.w, fv, -sz));
 }
 
 struct AppLavaMD : AppBase {
