@@ -518,10 +518,11 @@ static int region_eval(const region_view* rv, int64_t idx, int lane, int round, 
         const double q = r->table_out[b * P + j];
         /* Rodinia lavaMD pair term: r2 = rA.v + rB.v - dot(rA, rB),
            vij = exp(-a2 r2), f += qB (vij, 2 vij (rA - rB)); FMA form with
-           -a2 folded into rA (and into rB.v): x = (-a2 vA + -a2 vB) - dot(-a2 rA, rB) */
-        const double an = na2 * me[0], axn = na2 * me[1], ayn = na2 * me[2], azn = na2 * me[3];
-        const double dotn = fma(azn, o2[3], fma(ayn, o2[2], axn * o2[1]));
-        const double vij = lava_exp((an + na2 * o2[0]) - dotn);
+           -a2 folded into rA (and into rB.v): x = -a2 vA + (-a2 vB + dot(a2 rA, rB)) */
+        const double an = na2 * me[0], nax = -(na2 * me[1]), nay = -(na2 * me[2]), naz = -(na2 * me[3]);
+        /* an + (-a2 vB + -a2 rA.rB) as three FMAs onto -a2 vB (apps.cuh) */
+        const double sb = fma(naz, o2[3], fma(nay, o2[2], fma(nax, o2[1], na2 * o2[0])));
+        const double vij = lava_exp(an + sb);
         const double qv = q * vij;
         const double t = qv + qv;
         fv = fv + qv;

@@ -686,8 +686,11 @@ static __device__ __noinline__ double4 lava_box_contribution(const double* rv_ho
   const double4 me = *reinterpret_cast<const double4*>(rv_home);
   // exponent argument -a2 (vA + vB - dot) with -a2 folded into the home
   // particle (once) and into the staged vB (staging): 5 ops instead of 6
-  const double an = __dmul_rn(na2, me.x), axn = __dmul_rn(na2, me.y), ayn = __dmul_rn(na2, me.z),
-               azn = __dmul_rn(na2, me.w);
+  // -nax = na2 x etc.: the exponent argument is an + (-a2 vB - a2 rA.rB) as
+  // three FMAs onto the staged -a2 vB and one add (5 ops before: DMUL, two
+  // FMAs, add, subtract)
+  const double an = __dmul_rn(na2, me.x), nax = -__dmul_rn(na2, me.y), nay = -__dmul_rn(na2, me.z),
+               naz = -__dmul_rn(na2, me.w);
   double fv = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
 #ifndef HPAC_LAVA_UNROLL
 #define HPAC_LAVA_UNROLL 1  // measured: 1 (32.7 ms) < 4 (35.5) < 2 (36.5) at 32^3
@@ -698,8 +701,8 @@ static __device__ __noinline__ double4 lava_box_contribution(const double* rv_ho
     const double2 b01 = *reinterpret_cast<const double2*>(s + j * 4);
     const double2 b23 = *reinterpret_cast<const double2*>(s + j * 4 + 2);
     const double q2 = s[P * 4 + j];  // 2*qv, staged (exact doubling)
-    const double dotn = fma(azn, b23.y, fma(ayn, b23.x, __dmul_rn(axn, b01.y)));
-    const double vij = lava_exp(__dsub_rn(__dadd_rn(an, b01.x), dotn), etab);  // b01.x = -a2 vB
+    const double sb = fma(naz, b23.y, fma(nay, b23.x, fma(nax, b01.y, b01.x)));  // b01.x = -a2 vB
+    const double vij = lava_exp(__dadd_rn(an, sb), etab);
     // t = 2 q vij exactly as before (power-of-two scaling is exact); the
     // potential is accumulated doubled and halved once at the end: the
     // same bits as summing q*vij
