@@ -625,7 +625,8 @@ static __constant__ double kLavaC[6] = {HPAC_LAVA_L64, HPAC_LAVA_LN2_64_HI, HPAC
                                         0x1.5555555555555p-3};
 
 __device__ __forceinline__ double lava_exp(double x, const double* tab) {
-  const double kd = __dsub_rn(fma(x, kLavaC[0], HPAC_LAVA_SHIFT), HPAC_LAVA_SHIFT);
+  const double ts = fma(x, kLavaC[0], HPAC_LAVA_SHIFT);  // 1.5*2^52 + n: n in the low word
+  const double kd = __dsub_rn(ts, HPAC_LAVA_SHIFT);
   double r = fma(-kd, kLavaC[1], x);
   r = fma(-kd, kLavaC[2], r);
   double s = kLavaC[3];  // 1/120
@@ -634,7 +635,7 @@ __device__ __forceinline__ double lava_exp(double x, const double* tab) {
   s = fma(s, r, 0x1.0000000000000p-1);
   s = fma(s, r, 1.0);
   s = fma(s, r, 1.0);
-  const int n = (int)kd;
+  const int n = __double2loint(ts);  // == (int)kd, without an F2I
   const double t = __dmul_rn(tab[n & 63], s);
   const int k = n >> 6;  // floor(n / 64)
   // exact power-of-two scaling == ldexp while the result stays normal: add
