@@ -380,11 +380,16 @@ __global__ void __launch_bounds__(kStreamMaxT, HPAC_LANE_MINB) bs_lane_kernel(co
   if (TECH == HPAC_TECH_PERFO && (p.perfo_kind == HPAC_PERFO_INI || p.perfo_kind == HPAC_PERFO_FINI))
     trip = (int)trip_count(tid, G, p.n, p.steps);
 
-  unsigned c_total = 0, c_approx = 0, c_warp = 0, c_div = 0;
-  bool resident = false, app_error = false;
+  // per-step bookkeeping kept to what the directive needs: the total and
+  // warp-step counts follow from my_steps at the end (a segment has an active
+  // lane at step s iff s < its lanes' largest my_steps), and only
+  // thread-level decisions can split a segment (warp/team votes are uniform)
+  unsigned c_approx = 0, c_div = 0;
+  bool app_error = false;
   const double* src = p.region.in + tid * kRec;
-  double* dst = p.region.out ? p.region.out + tid : nullptr;
-  uint8_t* path = p.paths ? p.paths + tid : nullptr;
+  double* const out = p.region.out;
+  uint8_t* const paths = p.paths;
+  int64_t idx = tid;
 
   for (int step = 0; step < nsteps; ++step) {
     const bool active = step < my_steps;
@@ -414,7 +419,7 @@ __global__ void __launch_bounds__(kStreamMaxT, HPAC_LANE_MINB) bs_lane_kernel(co
       if (approx) {
         if (TECH == HPAC_TECH_TAF) {
           // TafState::emit_approx, taf.hpp:114-117
-          if (dst) __stcs(dst, last);
+          if (out) __stcs(out + idx, last);
           if (taf_mode == kTafPredicting && --taf_rem == 0) {
             taf_count = 0;
             taf_mode = kTafFilling;
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(kStreamMaxT, HPAC_LANE_MINB) bs_lane_kernel(co
         double v = 0.0;
         if (!bs_call(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3), __ldg(src + 4), v))
           app_error = true;
-        if (dst) __stcs(dst, v);
+        if (out) __stcs(out + idx, v);
         if (TECH == HPAC_TECH_TAF) {
           // TafState::observe_accurate, taf.hpp:94-108
 #pragma unroll
@@ -450,22 +455,26 @@ __global__ void __launch_bounds__(kStreamMaxT, HPAC_LANE_MINB) bs_lane_kernel(co
           }
         }
       }
-      c_total += 1;
       if (approx) c_approx += 1;
-      if (path) *path = approx ? 1 : 0;
+      if (paths) paths[idx] = approx ? 1 : 0;
     }
-    // ---- warp stats (cost.hpp:66-86)
-    const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
-    const unsigned bx = __ballot_sync(0xffffffffu, active && approx) & seg_mask;
-    if (lane == 0 && ba) {
-      resident = true;
-      c_warp += 1;
-      if (bx != 0 && bx != ba) c_div += 1;
+    // ---- divergent warp steps (cost.hpp:66-86): thread-level decisions only
+    if (TECH != kTechNoneStream && LEVEL == HPAC_LEVEL_THREAD) {
+      const unsigned ba = __ballot_sync(0xffffffffu, active) & seg_mask;
+      const unsigned bx = __ballot_sync(0xffffffffu, active && approx) & seg_mask;
+      if (lane == 0 && bx != 0 && bx != ba) c_div += 1;
     }
     src += G * kRec;
-    if (dst) dst += G;
-    if (path) path += G;
+    idx += G;
   }
+  // warp steps and resident warps of the logical warp (segment): the
+  // segment's largest my_steps, at its lane 0
+  int seg_steps = my_steps;
+  for (int o = 1; o < ws && o < 32; o <<= 1)
+    seg_steps = max(seg_steps, __shfl_xor_sync(0xffffffffu, seg_steps, o));
+  const unsigned c_total = (unsigned)my_steps;
+  const unsigned c_warp = lane == 0 ? (unsigned)seg_steps : 0u;
+  const bool resident = lane == 0 && seg_steps > 0;
 
   const unsigned long long s_total = warp_sum_u32(c_total);
   const unsigned long long s_approx = warp_sum_u32(c_approx);
