@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define HPAC_ABI_VERSION 3
+#define HPAC_ABI_VERSION 4 /* v4: hpac_run_region_host_teams; v3: status-returning all-reduce hooks */
 
 /* ---- status codes ------------------------------------------------------ */
 #define HPAC_OK 0

@@ -14,7 +14,7 @@ from paper_2308_16877_b200 import engine as E
 
 def test_library_exports_every_declared_symbol():
     lib = abi.lib()
-    assert lib.hpac_abi_version() == 3
+    assert lib.hpac_abi_version() == 4
     declared = abi.exported_symbols()
     assert len(declared) >= 15
     out = subprocess.run(["nm", "-D", "--defined-only", str(abi.LIB_PATH)], capture_output=True,
