@@ -87,6 +87,34 @@ __device__ __forceinline__ void team_lookup(const double* tab, int stride, int D
   }
 }
 
+// team_lookup's hit for 5-dimensional records without square roots:
+// sqrt_rn(ssq) <= thr  <=>  ssq <= thr2 (runtime.cu sqrt_threshold_square),
+// and a later slot replaces the hit iff its rounded distance is strictly
+// smaller: certain when its ssq is below the hit's by more than 2^-48
+// relative (a 2^-49 gap in the root, far above rounding), decided on the
+// rounded roots when the two ssq are that close.
+__device__ __forceinline__ int team_hit5(const double* tab, const double* in, int occ, double thr2) {
+  int hit = -1;
+  double hq = 0.0;
+  for (int s = 0; s < occ; ++s) {
+    double ssq = 0.0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      const double df = __dsub_rn(tab[s * 5 + c], in[c]);
+      ssq = __dadd_rn(ssq, __dmul_rn(df, df));
+    }
+    if (ssq <= thr2) {
+      bool take = hit < 0 || ssq < hq * (1.0 - 0x1p-48);
+      if (!take && ssq < hq) take = __dsqrt_rn(ssq) < __dsqrt_rn(hq);
+      if (take) {
+        hit = s;
+        hq = ssq;
+      }
+    }
+  }
+  return hit;
+}
+
 }  // namespace
 
 // Every lane of the team stores (engine.hpp:317,338); only an accumulating
@@ -1652,8 +1680,7 @@ __global__ void __launch_bounds__(128) binomial_decide_kernel(const EngineParams
         if (TECH == HPAC_TECH_IACT) {
           // one team-shared MemoTable (iact.hpp:58-145): a hit emits the
           // slot's output, a miss is inserted at the round-robin cursor
-          int hit, near;
-          team_lookup(tab, 1, 5, 5, inb + s * 5, occ, p.iact_thr, hit, near);
+          const int hit = team_hit5(tab, inb + s * 5, occ, p.iact_thr2);
           if (hit >= 0) {
             a = src[hit];
           } else {
