@@ -1663,6 +1663,12 @@ __global__ void __launch_bounds__(128) binomial_decide_kernel(const EngineParams
   const unsigned long long tpt = (unsigned long long)p.tpt, wpt = (unsigned long long)p.wpt;
   unsigned long long app = 0;
   int rr = 0, occ = 0;
+  // lane-parallel table (tsize <= 32): slot `lane` in registers
+  const bool lane_tab = p.tsize <= 32;
+  int width = 1;
+  while (width < p.tsize && width < 32) width <<= 1;
+  double ent[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  int sstep = -1;
   for (int64_t b0 = 0; b0 < trip; b0 += 32) {
     const int cnt = (int)(trip - b0 < 32 ? trip - b0 : 32);
     if (TECH == HPAC_TECH_IACT && lane < cnt) {
@@ -1672,7 +1678,73 @@ __global__ void __launch_bounds__(128) binomial_decide_kernel(const EngineParams
     }
     __syncwarp();
     int nm = 0, mbase = 0;
-    if (lane == 0) {
+    if (TECH == HPAC_TECH_IACT && lane_tab) {
+      // the team's table across the warp: lane e holds slot e (registers),
+      // every slot's distance is computed at once, and the hit (smallest
+      // rounded distance, lowest slot on ties: team_lookup's rule) comes
+      // from a butterfly over the slots
+      for (int s = 0; s < cnt; ++s) {
+        const int64_t step = b0 + s;
+        const int64_t item = team + step * G;
+        double x[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) x[d] = inb[s * 5 + d];
+        double q = 0.0;
+        bool cand = false;
+        if (lane < occ) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            const double df = __dsub_rn(ent[d], x[d]);
+            q = __dadd_rn(q, __dmul_rn(df, df));
+          }
+          cand = q <= p.iact_thr2;
+        }
+        int bi = lane;
+        for (int o = 1; o < width; o <<= 1) {
+          const double oq = __shfl_xor_sync(0xffffffffu, q, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const bool oc = __shfl_xor_sync(0xffffffffu, cand, o);
+          bool take_o;
+          if (!oc) take_o = false;
+          else if (!cand) take_o = true;
+          else if (oq < q * (1.0 - 0x1p-48)) take_o = true;
+          else if (q < oq * (1.0 - 0x1p-48)) take_o = false;
+          else {
+            const double da = __dsqrt_rn(q), db = __dsqrt_rn(oq);
+            take_o = db < da || (db == da && oi < bi);
+          }
+          if (take_o) {
+            q = oq;
+            bi = oi;
+            cand = true;
+          }
+        }
+        // lanes past `width` reduced among themselves: lane 0 holds the answer
+        cand = __shfl_sync(0xffffffffu, cand, 0);
+        bi = __shfl_sync(0xffffffffu, bi, 0);
+        const int hs = __shfl_sync(0xffffffffu, sstep, cand ? bi : 0);
+        int a = -1;
+        if (cand) {
+          a = hs;
+        } else {
+          if (lane == rr) {
+#pragma unroll
+            for (int d = 0; d < 5; ++d) ent[d] = x[d];
+            sstep = (int)step;
+          }
+          rr = rr + 1 == p.tsize ? 0 : rr + 1;
+          occ = occ + 1 < p.tsize ? occ + 1 : p.tsize;
+        }
+        if (lane == 0) {
+          wk.act[item] = a;
+          if (a == -1) ml[nm] = (int)item;
+          else app += tpt;
+          if (p.paths) p.paths[item] = a != -1 ? 1 : 0;
+        }
+        if (a == -1) ++nm;
+      }
+      if (lane == 0 && nm) mbase = (int)atomicAdd(&wk.ctr[0], (unsigned)nm);
+    } else if (lane == 0) {
       for (int s = 0; s < cnt; ++s) {
         const int64_t step = b0 + s;
         const int64_t item = team + step * G;

@@ -161,7 +161,8 @@ def test_binomial_one_step_by_hand():
     assert abs(out[0] - want) <= 1e-15 * want * 8
 
 
-@pytest.mark.parametrize("ipt,thr,tsize", [(8, 0.5, 4), (64, 0.5, 4), (64, 2.0, 4), (128, 0.5, 8), (300, 0.5, 2)])
+@pytest.mark.parametrize("ipt,thr,tsize", [(8, 0.5, 4), (64, 0.5, 4), (64, 2.0, 4), (128, 0.5, 8), (300, 0.5, 2),
+                                            (64, 0.5, 3), (64, 1.0, 5), (64, 0.3, 7), (128, 0.5, 12)])
 def test_binomial_iact_team_decisions_bit_exact(ipt, thr, tsize):
     steps = 64
     n = 96 * ipt
@@ -296,3 +297,21 @@ def test_binomial_american_put_grid_of_moneyness(steps):
     lr = E.run_region(E.GridConfig(m, 64, 32, 1), m, 1, E.binomial_region(dev(opts), steps, out), None)
     ok, worst = _rel_ok(out.cpu().numpy(), want)
     assert ok, worst
+
+
+@pytest.mark.parametrize("tsize", [16, 32, 40])
+def test_binomial_iact_large_tables_bit_exact(tsize):
+    # tables past the default 48 KiB arena (a larger shared_mem_budget):
+    # the decide kernel's lane-per-slot table up to 32 slots, the lane-0
+    # scan beyond
+    steps, ipt = 64, 64
+    n = 64 * ipt
+    opts = E.make_binomial_portfolio(n, 43)
+    grid, mapping = E.resolve_grid("binomial", n, items_per_thread=ipt)
+    grid.shared_mem_budget_bytes = 200 * 1024
+    d_opts = dev(opts)
+    _, exact, _ = _gpu_run(grid, n, mapping, lambda o: E.binomial_region(d_opts, steps, o), None)
+    spec = E.iact(tsize, 0.5, level="team")
+    lr, g_out, g_paths = _gpu_run(grid, n, mapping, lambda o: E.binomial_region(d_opts, steps, o), spec)
+    st, o_out, o_paths = _replay(grid, n, mapping, opts, exact, E.iact(tsize, 0.5, level="team"))
+    _compare(lr, st, g_out, o_out, g_paths, o_paths)
